@@ -1,0 +1,114 @@
+/*
+ * sigattn.h -- C ABI of libsigattn.so: padding-aware bidirectional sigmoid attention on B200
+ * (sm_100a), forward and backward.
+ *
+ * Operation (Eq. 2; Alg. 1-3):
+ *   O     = sigma(alpha * Q K^T + b) V                    per (batch z, head h)
+ *   P_ij  = sigma(alpha <q_i,k_j> + b_z) if i < n_q[z] and j < n_k[z], else 0   (Alg. 1)
+ *   dV    = P^T dO                                        (Alg. 3)
+ *   dS    = P (1 - P) (dO V^T)                            (Alg. 2; diagonal Jacobian P:358-365)
+ *   dQ    = alpha dS K,   dK = alpha dS^T Q               (Alg. 2; Alg. 3)
+ *   Rows i >= n_q[z] of O and dQ, and rows j >= n_k[z] of dK and dV, are written as exact 0
+ *   (P:593).
+ *
+ * Conventions shared by every entry point:
+ *   - Tensors are [B, H, N, d] contiguous (row-major), N = Nq for Q, O, dO, dQ and N = Nk for
+ *     K, V, dK, dV.  d in {64, 128}.  Element type bf16 or fp16 (sigattn_dtype).  All tensor
+ *     pointers are DEVICE pointers, 16-byte aligned, owned by the caller; the library never
+ *     frees or retains them beyond the call's stream work.
+ *   - seqlens_q / seqlens_k are DEVICE int32 [B] valid lengths (validity is a prefix).
+ *     NULL means "all valid".  Values are clamped to [0, N] on the device; n = 0 gives all-zero
+ *     rows.  Pad CONTENT must be finite (a tensor core computes 0 * NaN = NaN); with finite pad
+ *     the outputs are independent of it.
+ *   - All calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *     default stream).  No host synchronisation happens inside a call.  Calls are reentrant.
+ *   - Errors: a status code is returned and no exception crosses the ABI.  Host-detectable
+ *     argument errors return SIGATTN_EINVAL before anything is launched; launch failures return
+ *     SIGATTN_ECUDA.  sigattn_last_error() gives a thread-local message for the last failure.
+ */
+#ifndef SIGATTN_H_
+#define SIGATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { SIGATTN_BF16 = 0, SIGATTN_FP16 = 1 } sigattn_dtype;
+
+typedef enum {
+  SIGATTN_OK = 0,
+  SIGATTN_EINVAL = 1,        /* bad argument (shape, dtype, alignment, null pointer, ws size) */
+  SIGATTN_EUNSUPPORTED = 2,  /* valid request this build does not implement                 */
+  SIGATTN_ECUDA = 3,         /* a CUDA runtime / driver call or a launch failed             */
+  SIGATTN_EWORKSPACE = 4     /* workspace too small                                          */
+} sigattn_status;
+
+/* flags bitfield */
+enum {
+  SIGATTN_F_OUT_F32_PARTIAL = 1u << 1, /* fwd: o is float* (fp32, no cast) -- a partial O
+                                          for key-split context parallelism (A4)     */
+  SIGATTN_F_DQ_F32_PARTIAL = 1u << 2,  /* bwd: dq is float* fp32 alpha*dS K, not finalised
+                                          (for the CP reduce-scatter)                        */
+  SIGATTN_F_NO_ZERO_PAD_OUT = 1u << 3  /* caller does not need padded output rows zeroed     */
+};
+
+typedef struct {
+  int B, H;          /* batch, heads                                                     */
+  int Nq, Nk;        /* padded query / key lengths (Nq == Nk for self-attention)         */
+  int d;             /* head dimension: 64 or 128                                        */
+  int dtype;         /* sigattn_dtype                                                    */
+  const int32_t* seqlens_q; /* device [B] or NULL (all Nq valid)                          */
+  const int32_t* seqlens_k; /* device [B] or NULL (all Nk valid)                          */
+  float scale;       /* alpha; callers pass 1/sqrt(d) by convention              */
+  float bias;        /* scalar b, used when bias_per_seq == NULL (b = -log n)     */
+  const float* bias_per_seq; /* device [B] or NULL: per-sequence b in R^Z (Alg. 1)  */
+  unsigned flags;    /* SIGATTN_F_*                                                      */
+} sigattn_params;
+
+/* Forward (Alg. 1).  q [B,H,Nq,d], k/v [B,H,Nk,d], o [B,H,Nq,d] (fp32 if OUT_F32_PARTIAL).
+ * Fully padded query tiles are skipped and the key loop stops at n_k.     */
+sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k, const void* v,
+                           void* o, void* stream);
+
+/* Bytes of device workspace sigattn_bwd needs (an fp32 dQ accumulator [B,H,Nq,d] plus a
+ * small scheduling area).  Returns 0 for invalid params.                                     */
+size_t sigattn_bwd_workspace_bytes(const sigattn_params* p);
+
+/* Backward (Alg. 2 + Alg. 3, fused into one key-tile-owned pass: dK/dV accumulate on chip
+ * without atomics, dQ partials are reduced into the fp32 workspace, then finalised).
+ * dout [B,H,Nq,d]; dq [B,H,Nq,d] (fp32 if DQ_F32_PARTIAL); dk, dv [B,H,Nk,d].
+ * workspace: device, >= sigattn_bwd_workspace_bytes(p), 16-byte aligned, caller-owned.       */
+sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k, const void* v,
+                           const void* dout, void* dq, void* dk, void* dv, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* key_padding_mask [B,N] uint8 (1 = PAD, PyTorch convention) -> seqlens [B] int32 (device).
+ * Only prefix masks reduce to lengths: *nonprefix_flag (device int32) is set to 1 if any row
+ * has a valid token after a pad token, else 0.                                               */
+sigattn_status sigattn_mask_to_seqlens(const uint8_t* key_padding_mask, int B, int N,
+                                       int32_t* seqlens, int32_t* nonprefix_flag, void* stream);
+
+/* Valid-token FLOP credit (App. B.1): sum_b c * H * d * nq[b] * nk[b] with c = 4
+ * (forward) or 10 (backward).  HOST arrays, no GPU needed.  Returns -1 on bad arguments.      */
+int64_t sigattn_valid_flops(int B, int H, int d, const int32_t* host_nq, const int32_t* host_nk,
+                            int forward);
+
+/* Host mirror of the device work-list builder, for tests and schedulers: writes the items the
+ * forward (kind = 0, items = (b,h,q-tile), cost = key tiles) or backward (kind = 1, items =
+ * (b,h,k-tile), cost = query tiles) kernel visits, in visiting order (longest first, ties by
+ * b then h then tile).  Each item is 4 int32: {b, h, tile, cost}.  Returns the item count, or
+ * -1 on bad arguments; writes at most max_items.  tile = 128 rows.                            */
+int64_t sigattn_worklist_host(int kind, int B, int H, int Nq, int Nk, const int32_t* host_nq,
+                              const int32_t* host_nk, int32_t* items, int64_t max_items);
+
+const char* sigattn_last_error(void); /* thread-local message of the last failing call */
+const char* sigattn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SIGATTN_H_ */

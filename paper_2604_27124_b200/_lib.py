@@ -1,0 +1,84 @@
+"""ctypes binding of libsigattn.so (include/sigattn.h): argument marshalling only.
+
+Every step of the method runs inside the library's CUDA kernels.  If the library is missing
+this module raises -- there is no CPU or PyTorch fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libsigattn.so")
+
+SIGATTN_BF16 = 0
+SIGATTN_FP16 = 1
+SIGATTN_OK = 0
+SIGATTN_F_OUT_F32_PARTIAL = 1 << 1
+SIGATTN_F_DQ_F32_PARTIAL = 1 << 2
+SIGATTN_F_NO_ZERO_PAD_OUT = 1 << 3
+
+STATUS_NAMES = {0: "SIGATTN_OK", 1: "SIGATTN_EINVAL", 2: "SIGATTN_EUNSUPPORTED", 3: "SIGATTN_ECUDA",
+                4: "SIGATTN_EWORKSPACE"}
+
+EXPORTED = ["sigattn_fwd", "sigattn_bwd", "sigattn_bwd_workspace_bytes", "sigattn_mask_to_seqlens",
+            "sigattn_valid_flops", "sigattn_worklist_host", "sigattn_last_error", "sigattn_version"]
+
+
+class SigattnParams(ctypes.Structure):
+    _fields_ = [
+        ("B", ctypes.c_int), ("H", ctypes.c_int), ("Nq", ctypes.c_int), ("Nk", ctypes.c_int),
+        ("d", ctypes.c_int), ("dtype", ctypes.c_int),
+        ("seqlens_q", ctypes.c_void_p), ("seqlens_k", ctypes.c_void_p),
+        ("scale", ctypes.c_float), ("bias", ctypes.c_float),
+        ("bias_per_seq", ctypes.c_void_p), ("flags", ctypes.c_uint),
+    ]
+
+
+class SigattnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load():
+    """Load libsigattn.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: build it with `python -m paper_2604_27124_b200.build` "
+                          "or __graft_entry__.build() -- there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER(SigattnParams)
+    vp = ctypes.c_void_p
+    lib.sigattn_fwd.argtypes = [P, vp, vp, vp, vp, vp]
+    lib.sigattn_fwd.restype = ctypes.c_int
+    lib.sigattn_bwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    lib.sigattn_bwd.restype = ctypes.c_int
+    lib.sigattn_bwd_workspace_bytes.argtypes = [P]
+    lib.sigattn_bwd_workspace_bytes.restype = ctypes.c_size_t
+    lib.sigattn_mask_to_seqlens.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
+    lib.sigattn_mask_to_seqlens.restype = ctypes.c_int
+    lib.sigattn_valid_flops.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int]
+    lib.sigattn_valid_flops.restype = ctypes.c_int64
+    lib.sigattn_worklist_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          vp, vp, vp, ctypes.c_int64]
+    lib.sigattn_worklist_host.restype = ctypes.c_int64
+    lib.sigattn_last_error.restype = ctypes.c_char_p
+    lib.sigattn_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(status: int):
+    if status != SIGATTN_OK:
+        raise SigattnError(status, load().sigattn_last_error().decode())
+
+
+def make_params(B, H, Nq, Nk, d, dtype_code, seqlens_q_ptr, seqlens_k_ptr, scale, bias, bias_ptr, flags):
+    return SigattnParams(int(B), int(H), int(Nq), int(Nk), int(d), int(dtype_code), seqlens_q_ptr or None,
+                         seqlens_k_ptr or None, float(scale), float(bias), bias_ptr or None, int(flags))

@@ -1,0 +1,214 @@
+"""Python boundary of the sigmoid-attention hot path (same names as include/sigattn.h).
+
+Argument marshalling only: tensors are checked, device pointers and the current CUDA stream are
+handed to libsigattn.so, and every step of the method (work list, zero fill, the fwd / bwd
+kernels, dQ finalisation) runs in the library's kernels.  There is no CPU / PyTorch fallback.
+
+    O = sigma(alpha Q K^T + b) V     (Eq. 2; padding semantics Alg. 1)
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional, Union
+
+import torch
+
+from . import _lib
+
+BiasArg = Union[None, float, str, torch.Tensor]
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.SIGATTN_BF16
+    if t.dtype == torch.float16:
+        return _lib.SIGATTN_FP16
+    raise TypeError(f"sigattn: dtype {t.dtype} unsupported (bf16 / fp16)")
+
+
+def _check_qkv(q, k, v):
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not t.is_cuda:
+            raise ValueError(f"sigattn: {name} must be a CUDA tensor (no CPU fallback)")
+        if t.dim() != 4:
+            raise ValueError(f"sigattn: {name} must be [B, H, N, d]")
+        if not t.is_contiguous():
+            raise ValueError(f"sigattn: {name} must be contiguous [B, H, N, d]")
+    B, H, Nq, d = q.shape
+    if k.shape[:2] != (B, H) or k.shape[3] != d or v.shape != k.shape:
+        raise ValueError(f"sigattn: shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("sigattn: q, k, v must share a dtype")
+    return B, H, Nq, k.shape[2], d
+
+
+def _lens(t: Optional[torch.Tensor], B: int, device) -> Optional[torch.Tensor]:
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        t = torch.tensor(list(t), dtype=torch.int32)
+    t = t.to(device=device, dtype=torch.int32).contiguous()
+    if t.numel() != B:
+        raise ValueError("sigattn: seqlens must have B entries")
+    return t
+
+
+def resolve_bias(bias: BiasArg, Nk: int, seqlens_k: Optional[torch.Tensor], B: int, device):
+    """b = -log n.  None -> scalar -log(Nk) (padded length, reading R1);
+    'per_seq' -> device tensor -log(n_k[b]) (Alg. 1's b in R^Z); float; or a [B] tensor."""
+    if bias is None:
+        return -math.log(Nk), None
+    if isinstance(bias, str):
+        if bias != "per_seq":
+            raise ValueError("sigattn: bias must be None, a float, 'per_seq' or a [B] tensor")
+        n = seqlens_k.to(torch.float32) if seqlens_k is not None else torch.full((B,), float(Nk), device=device)
+        return 0.0, (-torch.log(torch.clamp(n, min=1.0))).contiguous()
+    if isinstance(bias, torch.Tensor):
+        t = bias.to(device=device, dtype=torch.float32).reshape(-1).contiguous()
+        if t.numel() == 1:
+            return float(t.item()), None
+        if t.numel() != B:
+            raise ValueError("sigattn: bias tensor must have 1 or B entries")
+        return 0.0, t
+    return float(bias), None
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return t.data_ptr() if t is not None else None
+
+
+def _stream_handle(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def sigattn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens_q=None, seqlens_k=None,
+                scale: Optional[float] = None, bias: BiasArg = None, out: Optional[torch.Tensor] = None,
+                out_f32: bool = False, zero_pad_out: bool = True) -> torch.Tensor:
+    """Forward (Alg. 1).  Returns O [B, H, Nq, d] in q.dtype (fp32 if out_f32: a CP partial)."""
+    lib = _lib.load()
+    B, H, Nq, Nk, d = _check_qkv(q, k, v)
+    sq = _lens(seqlens_q, B, q.device)
+    sk = _lens(seqlens_k, B, q.device) if seqlens_k is not None else sq if Nk == Nq else None
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    b_scalar, b_tensor = resolve_bias(bias, Nk, sk, B, q.device)
+    odt = torch.float32 if out_f32 else q.dtype
+    if out is None:
+        out = torch.empty((B, H, Nq, d), dtype=odt, device=q.device)
+    elif out.shape != (B, H, Nq, d) or out.dtype != odt or not out.is_contiguous():
+        raise ValueError("sigattn: bad out tensor")
+    flags = (_lib.SIGATTN_F_OUT_F32_PARTIAL if out_f32 else 0) | (0 if zero_pad_out else _lib.SIGATTN_F_NO_ZERO_PAD_OUT)
+    p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags)
+    _lib.check(lib.sigattn_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                               _stream_handle(q.device)))
+    return out
+
+
+def bwd_workspace_bytes(B, H, Nq, Nk, d, dtype=torch.bfloat16) -> int:
+    p = _lib.make_params(B, H, Nq, Nk, d, _lib.SIGATTN_BF16 if dtype == torch.bfloat16 else _lib.SIGATTN_FP16,
+                         None, None, 1.0, 0.0, None, 0)
+    return int(_lib.load().sigattn_bwd_workspace_bytes(ctypes.byref(p)))
+
+
+def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias: BiasArg = None,
+                dq=None, dk=None, dv=None, workspace: Optional[torch.Tensor] = None, dq_f32: bool = False):
+    """Backward (Alg. 2 + Alg. 3, fused).  Returns (dQ, dK, dV); dQ is fp32 if dq_f32 (CP partial)."""
+    lib = _lib.load()
+    B, H, Nq, Nk, d = _check_qkv(q, k, v)
+    if dout.shape != q.shape or dout.dtype != q.dtype or not dout.is_contiguous():
+        raise ValueError("sigattn: dout must match q")
+    sq = _lens(seqlens_q, B, q.device)
+    sk = _lens(seqlens_k, B, q.device) if seqlens_k is not None else sq if Nk == Nq else None
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    b_scalar, b_tensor = resolve_bias(bias, Nk, sk, B, q.device)
+    dq = torch.empty((B, H, Nq, d), dtype=torch.float32 if dq_f32 else q.dtype, device=q.device) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    flags = _lib.SIGATTN_F_DQ_F32_PARTIAL if dq_f32 else 0
+    p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags)
+    need = int(lib.sigattn_bwd_workspace_bytes(ctypes.byref(p)))
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+    _lib.check(lib.sigattn_bwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
+                               dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), workspace.data_ptr(), need,
+                               _stream_handle(q.device)))
+    return dq, dk, dv
+
+
+def sigattn_mask_to_seqlens(key_padding_mask: torch.Tensor, check_prefix: bool = True) -> torch.Tensor:
+    """PyTorch key_padding_mask [B, N] (True = pad) -> int32 valid lengths, on device."""
+    lib = _lib.load()
+    m = key_padding_mask.to(torch.uint8).contiguous()
+    B, N = m.shape
+    seqlens = torch.empty(B, dtype=torch.int32, device=m.device)
+    flag = torch.empty(1, dtype=torch.int32, device=m.device)
+    _lib.check(lib.sigattn_mask_to_seqlens(m.data_ptr(), B, N, seqlens.data_ptr(), flag.data_ptr(),
+                                           _stream_handle(m.device)))
+    if check_prefix and int(flag.item()) != 0:
+        raise ValueError("sigattn: key_padding_mask is not a prefix mask (valid tokens after padding)")
+    return seqlens
+
+
+def valid_flops(B: int, H: int, d: int, nq, nk, forward: bool) -> int:
+    """App. B.1 FLOP credit on valid tokens: sum_b {4|10} H d n_q[b] n_k[b]."""
+    import numpy as np
+    a = np.ascontiguousarray(np.asarray(nq, dtype=np.int32))
+    c = np.ascontiguousarray(np.asarray(nk, dtype=np.int32))
+    r = _lib.load().sigattn_valid_flops(int(B), int(H), int(d), a.ctypes.data, c.ctypes.data, 1 if forward else 0)
+    if r < 0:
+        raise ValueError("sigattn_valid_flops: bad arguments")
+    return int(r)
+
+
+def worklist_host(kind: int, B: int, H: int, Nq: int, Nk: int, nq, nk):
+    """Host mirror of the device work list: list of (b, h, tile, cost) in visiting order."""
+    import numpy as np
+    lib = _lib.load()
+    a = np.ascontiguousarray(np.asarray(nq, dtype=np.int32))
+    c = np.ascontiguousarray(np.asarray(nk, dtype=np.int32))
+    n = lib.sigattn_worklist_host(kind, B, H, Nq, Nk, a.ctypes.data, c.ctypes.data, None, 0)
+    if n < 0:
+        raise ValueError("sigattn_worklist_host: bad arguments")
+    out = np.zeros((max(n, 1), 4), dtype=np.int32)
+    lib.sigattn_worklist_host(kind, B, H, Nq, Nk, a.ctypes.data, c.ctypes.data, out.ctypes.data, n)
+    return [tuple(int(x) for x in r) for r in out[:n]]
+
+
+class SigmoidAttentionFn(torch.autograd.Function):
+    """Autograd op: saves q, k, v and the lengths -- never O or P (P is recomputed)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, seqlens_q, seqlens_k, scale, bias):
+        o = sigattn_fwd(q, k, v, seqlens_q, seqlens_k, scale, bias)
+        ctx.save_for_backward(q, k, v, seqlens_q, seqlens_k, bias if isinstance(bias, torch.Tensor) else None)
+        ctx.scale = scale
+        ctx.bias = None if isinstance(bias, torch.Tensor) else bias
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, sq, sk, bt = ctx.saved_tensors
+        bias = bt if bt is not None else ctx.bias
+        dq, dk, dv = sigattn_bwd(q, k, v, do.contiguous(), sq, sk, ctx.scale, bias)
+        return dq, dk, dv, None, None, None, None
+
+
+def sigmoid_attention(q, k, v, seqlens_q=None, seqlens_k=None, key_padding_mask=None,
+                      scale: Optional[float] = None, bias: BiasArg = None):
+    """O = sigma(scale * Q K^T + bias) V with padded keys at zero weight; differentiable.
+
+    q [B,H,Nq,d], k/v [B,H,Nk,d] (bf16/fp16, CUDA, contiguous).  Lengths as int32 [B] tensors,
+    or a PyTorch key_padding_mask [B, Nk] (True = pad; prefix masks only).
+    """
+    if key_padding_mask is not None:
+        if seqlens_k is not None:
+            raise ValueError("give seqlens or key_padding_mask, not both")
+        seqlens_k = sigattn_mask_to_seqlens(key_padding_mask)
+        if seqlens_q is None and q.shape[2] == k.shape[2]:
+            seqlens_q = seqlens_k
+    B = q.shape[0]
+    sq = _lens(seqlens_q, B, q.device)
+    sk = _lens(seqlens_k, B, q.device)
+    if sk is None and sq is not None and q.shape[2] == k.shape[2]:
+        sk = sq
+    return SigmoidAttentionFn.apply(q, k, v, sq, sk, scale, bias)

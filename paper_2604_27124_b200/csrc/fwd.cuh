@@ -1,0 +1,299 @@
+// fwd.cuh -- sm_100a forward kernel of padding-aware sigmoid attention (Alg. 1).
+//
+//   O[z, M, h, :] = sum over key tiles N < n_k[z] of  sigma(alpha Q_M K_N^T + b_z) masked  . V_N
+//
+// One CTA per SM (persistent), warp-specialised:
+//   warp 0      TMA producer: Q tile (double-buffered) and a K/V ring of kStages tiles
+//   warp 1      MMA issuer (one thread): S = Q K^T  (SS, both K-major)  -> TMEM S[2] (double buffer)
+//                                        O += P V   (TS, P from TMEM, V MN-major) -> TMEM O
+//   warp 2      TMEM allocator
+//   warps 4-11  two sigmoid warpgroups: WG g owns key columns [64g, 64g+64) of every S tile:
+//               tcgen05.ld S -> x = alpha s + b -> sigma -> key mask -> bf16 -> tcgen05.st P
+//               (P aliased onto the first half of its own S columns), then the epilogue for
+//               its half of the O columns (padded query rows written as exact 0).
+// Work items (b, h, q-tile) come from a device work list sorted longest-first (LPT), built
+// by sched.cuh from the device seqlens, so fully padded query tiles are never visited
+// and the key loop stops at ceil(n_k / 128) tiles.
+#pragma once
+#include "sm100.cuh"
+
+namespace sigattn {
+
+constexpr int kTile = 128;           // B_M = B_N = 128 (UMMA M = 128, one TMEM lane per row)
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct FwdArgs {
+  const int4* items;      // {b, h, tile, cost}
+  const int* n_items;
+  const int32_t* seqlens_q;
+  const int32_t* seqlens_k;
+  const float* bias_per_seq;
+  float bias;
+  float scale;
+  int B, H, Nq, Nk;
+  void* o;                // bf16/fp16 [B,H,Nq,D] or fp32 partial
+};
+
+template <int D>
+struct FwdCfg {
+  static constexpr int kStages = (D == 64) ? 4 : 2;
+  static constexpr int kSub = D / 64;                       // 64-column (128 B) swizzle atoms per row
+  static constexpr int kTileBytes = kTile * D * 2;          // one 128-row tile of Q, K or V
+  static constexpr int kQOff = 0;                           // Q[2]
+  static constexpr int kKOff = kQOff + 2 * kTileBytes;      // K[kStages]
+  static constexpr int kVOff = kKOff + kStages * kTileBytes;
+  static constexpr int kBarOff = kVOff + kStages * kTileBytes;
+  static constexpr int kNumBars = 2 + 2 + 3 * kStages + 2 + 2 + 2;
+  static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int kThreads = 384;
+  static constexpr uint32_t kTmemCols = 512;
+  // TMEM columns
+  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
+};
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+template <int D, bool kBf16, bool kOutF32>
+__global__ void __launch_bounds__(384, 1)
+sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
+  using C = FwdCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* q_full = bars + 0;          // [2]
+  uint64_t* q_empty = bars + 2;         // [2]
+  uint64_t* k_full = bars + 4;          // [kStages]
+  uint64_t* v_full = k_full + C::kStages;
+  uint64_t* kv_empty = v_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;  // [2]
+  uint64_t* p_full = s_full + 2;             // [2]
+  uint64_t* o_full = p_full + 2;             // [1]
+  uint64_t* o_empty = o_full + 1;            // [1]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+
+  const uint32_t warp = sm100::warp_id();
+  const uint32_t lane = sm100::lane_id();
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&q_full[i], 1);
+      sm100::mbar_init(&q_empty[i], 1);
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&p_full[i], 8);   // one arrival per sigmoid warp
+    }
+    for (int i = 0; i < C::kStages; ++i) {
+      sm100::mbar_init(&k_full[i], 1);
+      sm100::mbar_init(&v_full[i], 1);
+      sm100::mbar_init(&kv_empty[i], 1);
+    }
+    sm100::mbar_init(o_full, 1);
+    sm100::mbar_init(o_empty, 8);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmQ);
+    sm100::tma_prefetch_desc(&tmK);
+    sm100::tma_prefetch_desc(&tmV);
+  }
+  if (warp == 2) sm100::tmem_alloc<C::kTmemCols>(tmem_holder);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  const int n_items = *args.n_items;
+  const int BH = args.B * args.H;
+  (void)BH;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol_q = sm100::policy_evict_first();
+      const uint64_t pol_kv = sm100::policy_evict_last();
+      uint32_t kv_it = 0, c = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int4 item = args.items[it];
+        const int b = item.x, h = item.y, qt = item.z, nkt = item.w;
+        if (nkt <= 0) continue;
+        const int zh = b * args.H + h;
+        const uint32_t qb = c & 1, qph = (c >> 1) & 1;
+        sm100::mbar_wait(&q_empty[qb], qph ^ 1);
+        sm100::mbar_arrive_expect_tx(&q_full[qb], C::kTileBytes);
+        uint8_t* qs = smem + C::kQOff + qb * C::kTileBytes;
+#pragma unroll
+        for (int s = 0; s < C::kSub; ++s)
+          sm100::tma_load_3d(qs + s * (kTile * 128), &tmQ, &q_full[qb], s * 64, qt * kTile, zh, pol_q);
+        for (int j = 0; j < nkt; ++j, ++kv_it) {
+          const uint32_t st = kv_it % C::kStages, ph = (kv_it / C::kStages) & 1;
+          sm100::mbar_wait(&kv_empty[st], ph ^ 1);
+          uint8_t* ks = smem + C::kKOff + st * C::kTileBytes;
+          uint8_t* vs = smem + C::kVOff + st * C::kTileBytes;
+          sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
+#pragma unroll
+          for (int s = 0; s < C::kSub; ++s)
+            sm100::tma_load_3d(ks + s * (kTile * 128), &tmK, &k_full[st], s * 64, j * kTile, zh, pol_kv);
+          sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
+#pragma unroll
+          for (int s = 0; s < C::kSub; ++s)
+            sm100::tma_load_3d(vs + s * (kTile * 128), &tmV, &v_full[st], s * 64, j * kTile, zh, pol_kv);
+        }
+        ++c;
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 128, false, false);
+      constexpr uint32_t idesc_o = sm100::make_idesc_f16(kBf16, 128, D, false, true);
+      const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
+      const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
+      const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
+      uint32_t kv_it = 0, s_it = 0, c = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int nkt = args.items[it].w;
+        if (nkt <= 0) continue;
+        const uint32_t qb = c & 1;
+        sm100::mbar_wait(&q_full[qb], (c >> 1) & 1);
+        const uint32_t qa = q_base + qb * C::kTileBytes;
+        auto issue_s = [&](uint32_t kvi, uint32_t si) {
+          const uint32_t st = kvi % C::kStages;
+          sm100::mbar_wait(&k_full[st], (kvi / C::kStages) & 1);
+          sm100::tc_fence_after();
+          const uint32_t ka = k_base + st * C::kTileBytes;
+          const uint32_t d_s = tmem + ((si & 1) ? C::kColS1 : C::kColS0);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
+            sm100::mma_ss(d_s, sm100::make_sdesc_sw128(qa + off, 16, 1024),
+                          sm100::make_sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
+          }
+          sm100::mma_commit(&s_full[si & 1]);
+        };
+        issue_s(kv_it, s_it);
+        for (int j = 0; j < nkt; ++j) {
+          if (j + 1 < nkt) issue_s(kv_it + j + 1, s_it + j + 1);
+          const uint32_t si = s_it + j;
+          sm100::mbar_wait(&p_full[si & 1], (si >> 1) & 1);
+          if (j == 0) sm100::mbar_wait(o_empty, (c & 1) ^ 1);   // epilogue drained the previous O
+          const uint32_t kvi = kv_it + j;
+          const uint32_t st = kvi % C::kStages;
+          sm100::mbar_wait(&v_full[st], (kvi / C::kStages) & 1);
+          sm100::tc_fence_after();
+          const uint32_t va = v_base + st * C::kTileBytes;
+          const uint32_t p_col = (si & 1) ? C::kColS1 : C::kColS0;
+#pragma unroll
+          for (int kk = 0; kk < kTile / 16; ++kk) {
+            // P for keys [16kk, 16kk+16): WG g = kk/4 stored its 64 keys packed at S cols [64g, 64g+32)
+            const uint32_t a_col = p_col + (kk >> 2) * 64 + (kk & 3) * 8;
+            sm100::mma_ts(tmem + C::kColO, tmem + a_col,
+                          sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
+                          (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          sm100::mma_commit(&kv_empty[st]);
+        }
+        sm100::mma_commit(&q_empty[qb]);
+        sm100::mma_commit(o_full);
+        kv_it += nkt;
+        s_it += nkt;
+        ++c;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== sigmoid warpgroups + epilogue =====================
+    const uint32_t g = (warp - 4) >> 2;          // warpgroup: key columns [64g, 64g+64)
+    const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const uint32_t row = quarter * 32 + lane;    // tile row = TMEM lane
+    const uint32_t lane_addr = (quarter * 32) << 16;
+    uint32_t s_it = 0, c = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      const int b = item.x, h = item.y, qt = item.z, nkt = item.w;
+      if (nkt <= 0) continue;
+      const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
+      const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
+      const float bias = args.bias_per_seq ? args.bias_per_seq[b] : args.bias;
+      const float a2 = -args.scale * kLog2e;   // sigma(x) = 1 / (1 + 2^(-x log2 e))
+      const float b2 = -bias * kLog2e;
+      for (int j = 0; j < nkt; ++j) {
+        const uint32_t si = s_it + j;
+        const uint32_t scol = (si & 1) ? C::kColS1 : C::kColS0;
+        sm100::mbar_wait(&s_full[si & 1], (si >> 1) & 1);
+        sm100::tc_fence_after();
+        const int key0 = j * kTile + (int)g * 64;
+        const bool need_mask = key0 + 64 > nk;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t r[32];
+          sm100::tmem_ld32_sync(tmem + lane_addr + scol + g * 64 + ch * 32, r);
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float p0 = sm100::rcp_approx(1.0f + sm100::ex2_approx(fmaf(__uint_as_float(r[e]), a2, b2)));
+            float p1 = sm100::rcp_approx(1.0f + sm100::ex2_approx(fmaf(__uint_as_float(r[e + 1]), a2, b2)));
+            if (need_mask) {
+              const int kidx = key0 + ch * 32 + e;
+              p0 = (kidx < nk) ? p0 : 0.0f;
+              p1 = (kidx + 1 < nk) ? p1 : 0.0f;
+            }
+            pk[e >> 1] = sm100::pack2<kBf16>(p0, p1);
+          }
+          sm100::tmem_st16(tmem + lane_addr + scol + g * 64 + ch * 16, pk);
+        }
+        sm100::tmem_wait_st();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&p_full[si & 1]);
+      }
+      s_it += nkt;
+      // ---- epilogue: O rows of this q tile, columns [g*D/2, g*D/2 + D/2)
+      sm100::mbar_wait(o_full, c & 1);
+      sm100::tc_fence_after();
+      constexpr int kHalf = D / 2;
+      uint32_t ov[kHalf];
+#pragma unroll
+      for (int cc = 0; cc < kHalf / 32; ++cc) {
+        uint32_t r[32];
+        sm100::tmem_ld32_sync(tmem + lane_addr + C::kColO + g * kHalf + cc * 32, r);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) ov[cc * 32 + e] = r[e];
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(o_empty);
+      const int qrow = qt * kTile + (int)row;
+      if (qrow < args.Nq) {
+        const bool valid = qrow < nq;
+        const size_t off = ((size_t)(b * args.H + h) * args.Nq + qrow) * D + g * kHalf;
+        if constexpr (kOutF32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + off);
+#pragma unroll
+          for (int e = 0; e < kHalf; e += 4) {
+            float4 w = valid ? make_float4(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1]),
+                                           __uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3]))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            dst[e >> 2] = w;
+          }
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + off);
+#pragma unroll
+          for (int e = 0; e < kHalf; e += 8) {
+            uint4 w;
+            w.x = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 0]), __uint_as_float(ov[e + 1])) : 0u;
+            w.y = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3])) : 0u;
+            w.z = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 4]), __uint_as_float(ov[e + 5])) : 0u;
+            w.w = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 6]), __uint_as_float(ov[e + 7])) : 0u;
+            dst[e >> 3] = w;
+          }
+        }
+      }
+      ++c;
+    }
+  }
+
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+}
+
+}  // namespace sigattn

@@ -1,0 +1,348 @@
+// sigattn.cu -- C-ABI host side of libsigattn.so (declared in include/sigattn.h).
+// Validation, TMA descriptor encoding, workspace layout and kernel launches.  No computation of
+// the method happens on the host; every step runs in the kernels of fwd.cuh / bwd.cuh / sched.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sigattn.h"
+#include "bwd.cuh"
+#include "fwd.cuh"
+#include "sched.cuh"
+
+using namespace sigattn;
+
+namespace {
+
+thread_local std::string g_err;
+
+sigattn_status fail(sigattn_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(SIGATTN_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link dependency).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 3-D view {d (inner), rows, B*H} of a [B, H, rows, d] tensor; box {64 elements = 128 B, 128, 1},
+// 128-byte swizzle: exactly the UMMA K-major / MN-major SWIZZLE_128B atom.  Rows past `rows`
+// read as zero (OOB fill), so a ragged last tile never touches another head's data.
+sigattn_status make_tmap(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int elem_bytes, int d, int rows,
+                         int bh) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(SIGATTN_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)bh};
+  cuuint64_t strides[2] = {(cuuint64_t)d * elem_bytes, (cuuint64_t)d * elem_bytes * rows};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SIGATTN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return SIGATTN_OK;
+}
+
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+sigattn_status check_params(const sigattn_params* p) {
+  if (!p) return fail(SIGATTN_EINVAL, "params is NULL");
+  if (p->B <= 0 || p->H <= 0 || p->Nq <= 0 || p->Nk <= 0)
+    return fail(SIGATTN_EINVAL, "B, H, Nq, Nk must be positive");
+  if (p->d != 64 && p->d != 128) return fail(SIGATTN_EINVAL, "d must be 64 or 128");
+  if (p->dtype != SIGATTN_BF16 && p->dtype != SIGATTN_FP16) return fail(SIGATTN_EINVAL, "dtype must be bf16 or fp16");
+  if (p->B > kMaxSchedB) return fail(SIGATTN_EUNSUPPORTED, "B > 4096 sequences per call");
+  const long long bh = (long long)p->B * p->H;
+  if (bh > 65535) return fail(SIGATTN_EUNSUPPORTED, "B*H > 65535");
+  if (bh * std::max(p->Nq, p->Nk) * (long long)p->d >= (1ll << 40)) return fail(SIGATTN_EINVAL, "tensor too large");
+  if (!(p->scale == p->scale)) return fail(SIGATTN_EINVAL, "scale is NaN");
+  return SIGATTN_OK;
+}
+
+template <typename K>
+sigattn_status set_smem(K kernel, int bytes) {
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return SIGATTN_OK;
+}
+
+sigattn_status launch_worklist(int kind, const sigattn_params* p, int4* items, int* n_items, cudaStream_t s) {
+  const int smem = 4 * p->B * (int)sizeof(int);
+  if (smem > 48 * 1024) {
+    static bool set = false;
+    if (!set) {
+      CUDA_TRY(cudaFuncSetAttribute(build_worklist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      set = true;
+    }
+  }
+  build_worklist_kernel<<<1, kSchedThreads, smem, s>>>(kind, p->B, p->H, p->Nq, p->Nk, p->seqlens_q, p->seqlens_k,
+                                                        items, n_items);
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+sigattn_status launch_zero_rows(void* out, int row_bytes, const sigattn_params* p, int N, const int32_t* lens,
+                                const int32_t* gate, int gate_N, int mode, cudaStream_t s) {
+  dim3 grid(std::max(1, std::min(64, cdiv((long long)N * row_bytes / 16, 256))), p->B * p->H);
+  zero_rows_kernel<<<grid, 256, 0, s>>>(out, row_bytes, p->B, p->H, N, lens, gate, gate_N, mode);
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+template <int D, bool kBf16, bool kF32>
+sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k, const void* v, void* o,
+                          const int4* items, const int* n_items, int max_items, cudaStream_t s) {
+  const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tq, tk, tv;
+  const int bh = p->B * p->H;
+  sigattn_status st;
+  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
+  FwdArgs a;
+  a.items = items;
+  a.n_items = n_items;
+  a.seqlens_q = p->seqlens_q;
+  a.seqlens_k = p->seqlens_k;
+  a.bias_per_seq = p->bias_per_seq;
+  a.bias = p->bias;
+  a.scale = p->scale;
+  a.B = p->B;
+  a.H = p->H;
+  a.Nq = p->Nq;
+  a.Nk = p->Nk;
+  a.o = o;
+  using C = FwdCfg<D>;
+  auto kern = sigattn_fwd_kernel<D, kBf16, kF32>;
+  if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
+  const int grid = std::max(1, std::min(num_sms(), max_items));
+  kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, a);
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+template <int D, bool kBf16>
+sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
+                          float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
+                          cudaStream_t s) {
+  const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tq, tk, tv, tdo;
+  const int bh = p->B * p->H;
+  sigattn_status st;
+  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  BwdArgs a;
+  a.items = items;
+  a.n_items = n_items;
+  a.seqlens_q = p->seqlens_q;
+  a.seqlens_k = p->seqlens_k;
+  a.bias_per_seq = p->bias_per_seq;
+  a.bias = p->bias;
+  a.scale = p->scale;
+  a.B = p->B;
+  a.H = p->H;
+  a.Nq = p->Nq;
+  a.Nk = p->Nk;
+  a.dq_acc = dq_acc;
+  a.dk = dk;
+  a.dv = dv;
+  using C = BwdCfg<D>;
+  auto kern = sigattn_bwd_kernel<D, kBf16>;
+  if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
+  const int grid = std::max(1, std::min(num_sms(), max_items));
+  kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+const char* sigattn_last_error(void) { return g_err.c_str(); }
+
+const char* sigattn_version(void) { return "sigattn-b200 0.1 (sm_100a tcgen05/TMEM/TMA)"; }
+
+int64_t sigattn_valid_flops(int B, int H, int d, const int32_t* host_nq, const int32_t* host_nk, int forward) {
+  if (B <= 0 || H <= 0 || d <= 0 || !host_nq || !host_nk) return -1;
+  const int64_t c = forward ? 4 : 10;  // App. B.1: fwd 4 b h n^2 d, bwd 2.5x
+  int64_t s = 0;
+  for (int b = 0; b < B; ++b) {
+    if (host_nq[b] < 0 || host_nk[b] < 0) return -1;
+    s += (int64_t)host_nq[b] * (int64_t)host_nk[b];
+  }
+  return c * (int64_t)H * (int64_t)d * s;
+}
+
+int64_t sigattn_worklist_host(int kind, int B, int H, int Nq, int Nk, const int32_t* host_nq, const int32_t* host_nk,
+                              int32_t* items, int64_t max_items) {
+  if ((kind != 0 && kind != 1) || B <= 0 || H <= 0 || Nq <= 0 || Nk <= 0) return -1;
+  std::vector<int> cost(B), nt(B), order(B);
+  for (int b = 0; b < B; ++b) {
+    int nq = host_nq ? host_nq[b] : Nq, nk = host_nk ? host_nk[b] : Nk;
+    nq = std::min(std::max(nq, 0), Nq);
+    nk = std::min(std::max(nk, 0), Nk);
+    const int tq = (nq + 127) / 128, tk = (nk + 127) / 128;
+    cost[b] = kind == 0 ? tk : tq;
+    nt[b] = cost[b] == 0 ? 0 : (kind == 0 ? tq : tk);
+    order[b] = b;
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost[x] > cost[y]; });
+  int64_t n = 0;
+  for (int r = 0; r < B; ++r) {
+    const int b = order[r];
+    for (int h = 0; h < H; ++h)
+      for (int t = 0; t < nt[b]; ++t, ++n)
+        if (items && n < max_items) {
+          items[4 * n + 0] = b;
+          items[4 * n + 1] = h;
+          items[4 * n + 2] = t;
+          items[4 * n + 3] = cost[b];
+        }
+  }
+  return n;
+}
+
+sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k, const void* v, void* o,
+                           void* stream) {
+  sigattn_status st = check_params(p);
+  if (st != SIGATTN_OK) return st;
+  if (!q || !k || !v || !o) return fail(SIGATTN_EINVAL, "null tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(SIGATTN_EINVAL, "tensor pointers must be 16-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool f32 = (p->flags & SIGATTN_F_OUT_F32_PARTIAL) != 0;
+  const int elem_out = f32 ? 4 : 2;
+  const int max_items = p->B * p->H * cdiv(p->Nq, 128);
+  // stream-ordered scratch for the work list (pool-cached by the CUDA runtime)
+  void* scratch = nullptr;
+  const size_t bytes = 16 + (size_t)max_items * sizeof(int4);
+  CUDA_TRY(cudaMallocAsync(&scratch, bytes, s));
+  int* n_items = reinterpret_cast<int*>(scratch);
+  int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(scratch) + 16);
+  st = launch_worklist(0, p, items, n_items, s);
+  if (st == SIGATTN_OK && !(p->flags & SIGATTN_F_NO_ZERO_PAD_OUT))
+    st = launch_zero_rows(o, p->d * elem_out, p, p->Nq, p->seqlens_q, p->seqlens_k, p->Nk, 0, s);
+  if (st == SIGATTN_OK) {
+    const bool bf = p->dtype == SIGATTN_BF16;
+    if (p->d == 64) {
+      if (bf) st = f32 ? launch_fwd<64, true, true>(p, q, k, v, o, items, n_items, max_items, s)
+                       : launch_fwd<64, true, false>(p, q, k, v, o, items, n_items, max_items, s);
+      else st = f32 ? launch_fwd<64, false, true>(p, q, k, v, o, items, n_items, max_items, s)
+                    : launch_fwd<64, false, false>(p, q, k, v, o, items, n_items, max_items, s);
+    } else {
+      if (bf) st = f32 ? launch_fwd<128, true, true>(p, q, k, v, o, items, n_items, max_items, s)
+                       : launch_fwd<128, true, false>(p, q, k, v, o, items, n_items, max_items, s);
+      else st = f32 ? launch_fwd<128, false, true>(p, q, k, v, o, items, n_items, max_items, s)
+                    : launch_fwd<128, false, false>(p, q, k, v, o, items, n_items, max_items, s);
+    }
+  }
+  cudaError_t fe = cudaFreeAsync(scratch, s);
+  if (st == SIGATTN_OK && fe != cudaSuccess) return fail(SIGATTN_ECUDA, cudaGetErrorString(fe));
+  return st;
+}
+
+size_t sigattn_bwd_workspace_bytes(const sigattn_params* p) {
+  if (check_params(p) != SIGATTN_OK) return 0;
+  const size_t acc = (size_t)p->B * p->H * p->Nq * p->d * sizeof(float);
+  const size_t items = 16 + (size_t)p->B * p->H * cdiv(p->Nk, 128) * sizeof(int4);
+  return align_up(acc, 256) + align_up(items, 256);
+}
+
+sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
+                           void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, void* stream) {
+  sigattn_status st = check_params(p);
+  if (st != SIGATTN_OK) return st;
+  if (!q || !k || !v || !dout || !dq || !dk || !dv || !workspace) return fail(SIGATTN_EINVAL, "null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dq) || !aligned16(dk) ||
+      !aligned16(dv) || !aligned16(workspace))
+    return fail(SIGATTN_EINVAL, "pointers must be 16-byte aligned");
+  const size_t need = sigattn_bwd_workspace_bytes(p);
+  if (workspace_bytes < need)
+    return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  if (p->d != 64) return fail(SIGATTN_EUNSUPPORTED, "backward: d = 128 not implemented in this build");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool dq_f32 = (p->flags & SIGATTN_F_DQ_F32_PARTIAL) != 0;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  const size_t acc_bytes = align_up((size_t)p->B * p->H * p->Nq * p->d * sizeof(float), 256);
+  float* dq_acc = dq_f32 ? reinterpret_cast<float*>(dq) : reinterpret_cast<float*>(ws);
+  int* n_items = reinterpret_cast<int*>(ws + acc_bytes);
+  int4* items = reinterpret_cast<int4*>(ws + acc_bytes + 16);
+  const int max_items = p->B * p->H * cdiv(p->Nk, 128);
+  const int row16 = p->d * 2;
+  if ((st = launch_worklist(1, p, items, n_items, s)) != SIGATTN_OK) return st;
+  // dQ accumulator: valid rows zeroed (padded rows are never touched unless dq is the fp32 output)
+  if (dq_f32) {
+    CUDA_TRY(cudaMemsetAsync(dq, 0, (size_t)p->B * p->H * p->Nq * p->d * sizeof(float), s));
+  } else if ((st = launch_zero_rows(dq_acc, p->d * 4, p, p->Nq, p->seqlens_q, nullptr, -1, 1, s)) != SIGATTN_OK) {
+    return st;
+  }
+  if ((st = launch_zero_rows(dk, row16, p, p->Nk, p->seqlens_k, p->seqlens_q, p->Nq, 0, s)) != SIGATTN_OK) return st;
+  if ((st = launch_zero_rows(dv, row16, p, p->Nk, p->seqlens_k, p->seqlens_q, p->Nq, 0, s)) != SIGATTN_OK) return st;
+  const bool bf = p->dtype == SIGATTN_BF16;
+  st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s)
+          : launch_bwd<64, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s);
+  if (st != SIGATTN_OK) return st;
+  if (!dq_f32) {
+    const long long total8 = (long long)p->B * p->H * p->Nq * p->d / 8;
+    const int grid = (int)std::min<long long>(4LL * num_sms(), (total8 + 255) / 256);
+    if (bf)
+      dq_finalize_kernel<true><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
+                                                    p->seqlens_q, total8);
+    else
+      dq_finalize_kernel<false><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
+                                                     p->seqlens_q, total8);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return SIGATTN_OK;
+}
+
+sigattn_status sigattn_mask_to_seqlens(const uint8_t* key_padding_mask, int B, int N, int32_t* seqlens,
+                                       int32_t* nonprefix_flag, void* stream) {
+  if (!key_padding_mask || !seqlens || !nonprefix_flag || B <= 0 || N <= 0)
+    return fail(SIGATTN_EINVAL, "bad mask_to_seqlens arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaMemsetAsync(nonprefix_flag, 0, sizeof(int32_t), s));
+  mask_to_seqlens_kernel<<<B, 256, 0, s>>>(key_padding_mask, N, seqlens, nonprefix_flag);
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+}  // extern "C"

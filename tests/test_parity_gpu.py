@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same inputs.
+
+Bar (BASELINE.json north star): max|gpu - ref| / max|ref| <= 1e-2 for bf16 (O, dQ, dK, dV) and
+<= 2e-3 for the fp16 forward; padded rows exactly 0; finite pad content never changes O, dK, dV.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2604_27124_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 1e-2
+FP16_FWD_TOL = 2e-3
+
+
+def _sa():
+    import paper_2604_27124_b200 as sa
+    return sa
+
+
+def f64(t):
+    return t.detach().to(torch.float64).cpu().numpy()
+
+
+def relerr(got, ref):
+    den = np.abs(ref).max()
+    if den == 0:
+        return float(np.abs(got).max())
+    return float(np.abs(got - ref).max() / den)
+
+
+def run_case(cfg, bias=None, check_bwd=True, pad=None, tol=BF16_TOL):
+    sa = _sa()
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda", pad=pad)
+    alpha = 1.0 / math.sqrt(cfg.d)
+    b = -math.log(cfg.N_k) if bias is None else bias
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b)
+    torch.cuda.synchronize()
+    bias_np = np.full(cfg.B, b) if np.isscalar(b) else b.double().cpu().numpy()
+    ro = oracle.fwd(f64(q), f64(k), f64(v), cfg.nq, cfg.nk, alpha, bias_np)
+    e = relerr(f64(o), ro)
+    assert e <= tol, f"O rel err {e}"
+    for bb in range(cfg.B):
+        assert torch.all(o[bb, :, cfg.nq[bb]:] == 0), "padded query rows must be exactly 0"
+    res = {"o": e}
+    if check_bwd:
+        dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b)
+        torch.cuda.synchronize()
+        rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, alpha, bias_np)
+        for name, got, ref in (("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+            err = relerr(f64(got), ref)
+            res[name] = err
+            assert err <= BF16_TOL, f"{name} rel err {err}"
+        for bb in range(cfg.B):
+            assert torch.all(dq[bb, :, cfg.nq[bb]:] == 0)
+            assert torch.all(dk[bb, :, cfg.nk[bb]:] == 0) and torch.all(dv[bb, :, cfg.nk[bb]:] == 0)
+    return res
+
+
+def test_c1_bf16_fwd_bwd():
+    """BASELINE config 1: B=2 H=2 N=256 d=64, lengths {256, 97}, b = -log N, fwd+bwd vs oracle."""
+    r = run_case(I.C1)
+    print("C1 bf16", r)
+
+
+def test_c1_fp16_fwd():
+    r = run_case(I.C1_FP16, check_bwd=False, tol=FP16_FWD_TOL)
+    print("C1 fp16", r)
+
+
+def test_c1_fp16_bwd():
+    run_case(I.C1_FP16, check_bwd=True, tol=FP16_FWD_TOL)
+
+
+@pytest.mark.parametrize("cfg", [
+    I.Config("ragged_N200", B=4, H=3, N=200, d=64, lengths=[200, 1, 129, 127], seed=3),
+    I.Config("ragged_N384", B=3, H=2, N=384, d=64, lengths=[384, 255, 257], seed=4),
+    I.Config("zero_len", B=3, H=2, N=256, d=64, lengths=[0, 256, 5], seed=5),
+    I.Config("unpadded_N512", B=1, H=4, N=512, d=64, seed=6),
+    I.Config("many_short", B=40, H=2, N=128, d=64, lengths=[1 + (7 * i) % 128 for i in range(40)], seed=7),
+])
+def test_ragged_and_edge_cases(cfg):
+    run_case(cfg)
+
+
+def test_cross_lengths_nq_ne_nk():
+    cfg = I.Config("cross", B=3, H=2, N=320, d=64, lengths=[320, 100, 7], Nk=200, lengths_k=[200, 150, 1], seed=8)
+    run_case(cfg)
+
+
+def test_per_sequence_bias():
+    cfg = I.Config("perseq", B=3, H=2, N=256, d=64, lengths=[256, 60, 200], seed=9)
+    b = -torch.log(torch.tensor(cfg.nk, dtype=torch.float32)).cuda()
+    run_case(cfg, bias=b)
+
+
+@pytest.mark.parametrize("cfg", [
+    I.Config("d128", B=2, H=2, N=256, d=128, lengths=[256, 97], seed=10),
+    I.Config("d128_ragged", B=3, H=2, N=300, d=128, lengths=[300, 129, 1], seed=11),
+])
+def test_d128_forward(cfg):
+    run_case(cfg, check_bwd=False)
+
+
+def test_d128_fp16_forward():
+    cfg = I.Config("d128f16", B=2, H=2, N=256, d=128, lengths=[256, 97], dtype="fp16", seed=12)
+    run_case(cfg, check_bwd=False, tol=FP16_FWD_TOL)
+
+
+def test_pad_independence_bitwise():
+    """Finite pad content (0 vs 1e3 vs random) leaves O, dK, dV bitwise equal; dQ within tol."""
+    sa = _sa()
+    cfg = I.Config("padind", B=3, H=2, N=256, d=64, lengths=[256, 97, 130], seed=13)
+    outs = []
+    for pad in (None, 1e3, "random"):
+        q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda", pad=pad)
+        o = sa.sigattn_fwd(q, k, v, nq, nk)
+        dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk)
+        outs.append((o, dq, dk, dv))
+    for o, dq, dk, dv in outs[1:]:
+        assert torch.equal(o, outs[0][0])
+        assert torch.equal(dk, outs[0][2]) and torch.equal(dv, outs[0][3])
+        assert relerr(f64(dq), f64(outs[0][1])) < 1e-2
+
+
+def test_forward_deterministic():
+    sa = _sa()
+    q, k, v, do, nq, nk = I.make_inputs(I.C1, "cuda")
+    o1 = sa.sigattn_fwd(q, k, v, nq, nk)
+    o2 = sa.sigattn_fwd(q, k, v, nq, nk)
+    assert torch.equal(o1, o2)
+
+
+def test_cp_partial_sum_fp32():
+    """Key-split partials (fp32 out) summed == unsplit O (A4) within bf16 tolerance."""
+    sa = _sa()
+    cfg = I.Config("cp", B=1, H=2, N=512, d=64, seed=14)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    b = -math.log(512)
+    full = sa.sigattn_fwd(q, k, v, None, None, None, b, out_f32=True)
+    parts = [sa.sigattn_fwd(q, k[:, :, lo:lo + 128].contiguous(), v[:, :, lo:lo + 128].contiguous(), None, None,
+                            None, b, out_f32=True) for lo in range(0, 512, 128)]
+    s = sum(parts)
+    ro = oracle.fwd(f64(q), f64(k), f64(v), [512], [512], 1 / 8, [b])
+    assert relerr(f64(s), ro) <= BF16_TOL
+    assert relerr(f64(full), ro) <= BF16_TOL
+
+
+def test_autograd_and_mask_path():
+    sa = _sa()
+    cfg = I.Config("ag", B=2, H=2, N=256, d=64, lengths=[256, 77], seed=15)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    mask = torch.arange(256, device="cuda")[None, :] >= nk[:, None]
+    assert torch.equal(sa.sigattn_mask_to_seqlens(mask), nk)
+    bad = mask.clone(); bad[0, 3] = True
+    with pytest.raises(ValueError):
+        sa.sigattn_mask_to_seqlens(bad)
+    qq, kk, vv = (t.clone().requires_grad_(True) for t in (q, k, v))
+    o = sa.sigmoid_attention(qq, kk, vv, key_padding_mask=mask)
+    o.backward(do)
+    alpha = 1 / 8
+    bias = np.full(2, -math.log(256))
+    ro = oracle.fwd(f64(q), f64(k), f64(v), cfg.nq, cfg.nk, alpha, bias)
+    rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, alpha, bias)
+    assert relerr(f64(o), ro) <= BF16_TOL
+    for got, ref in ((qq.grad, rdq), (kk.grad, rdk), (vv.grad, rdv)):
+        assert relerr(f64(got), ref) <= BF16_TOL
+
+
+def _sampled_rows(n, N, rng, k=96):
+    """Boundary rows of every tile around n plus random rows."""
+    rows = {0, max(n - 1, 0), min(n, N - 1), N - 1}
+    for t in range(0, N, 128):
+        rows.update({t, min(t + 127, N - 1)})
+    rows.update(rng.integers(0, N, size=k).tolist())
+    return sorted(rows)
+
+
+def test_c3_full_size_sampled():
+    """C3 (B=32 N=8192 H=12 d=64 jagged) at full size, in the bench's launch configuration:
+    sampled rows of several (b, h) against the row-sampled oracle."""
+    sa = _sa()
+    cfg = I.C3
+    q, k, v, do, nq, nk = I.make_inputs_gpu_fast(cfg, "cuda")
+    alpha, b = 1 / 8, -math.log(8192)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b)
+    dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    bias = np.full(cfg.B, b)
+    for (bb, hh) in [(30, 0), (30, 11), (24, 5), (0, 3), (22, 7)]:
+        qs, ks, vs, dos = (f64(t[bb:bb + 1, hh:hh + 1]) for t in (q, k, v, do))
+        nqb, nkb = [cfg.nq[bb]], [cfg.nk[bb]]
+        rows = _sampled_rows(cfg.nq[bb], cfg.N, rng)
+        ro = oracle.fwd_rows(qs, ks, vs, 0, 0, rows, nqb, nkb, alpha, [b])
+        rdq = oracle.dq_rows(qs, ks, vs, dos, 0, 0, rows, nqb, nkb, alpha, [b])
+        rdk, rdv = oracle.dkdv_rows(qs, ks, vs, dos, 0, 0, rows, nqb, nkb, alpha, [b])
+        for name, got, ref in (("o", o, ro), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+            g = f64(got[bb, hh])[rows]
+            err = relerr(g, ref)
+            assert err <= BF16_TOL, f"{name} (b={bb}, h={hh}) rel err {err}"
