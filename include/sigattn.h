@@ -104,6 +104,14 @@ int64_t sigattn_valid_flops(int B, int H, int d, const int32_t* host_nq, const i
 int64_t sigattn_worklist_host(int kind, int B, int H, int Nq, int Nk, const int32_t* host_nq,
                               const int32_t* host_nk, int32_t* items, int64_t max_items);
 
+/* Instrumentation (bench / tests).  sigattn_launch_count(): number of kernels this library has
+ * launched in this process so far (all entry points).  sigattn_set_profile_events(): thread-local;
+ * when an event pair is non-NULL, the next sigattn_fwd / sigattn_bwd calls on this thread record
+ * `start` immediately before and `stop` immediately after their main attention kernel, on the
+ * call's stream (cudaEvent_t passed as void*).  Pass NULLs to disable.                          */
+int64_t sigattn_launch_count(void);
+void sigattn_set_profile_events(void* fwd_start, void* fwd_stop, void* bwd_start, void* bwd_stop);
+
 const char* sigattn_last_error(void); /* thread-local message of the last failing call */
 const char* sigattn_version(void);
 

@@ -22,7 +22,8 @@ STATUS_NAMES = {0: "SIGATTN_OK", 1: "SIGATTN_EINVAL", 2: "SIGATTN_EUNSUPPORTED",
                 4: "SIGATTN_EWORKSPACE"}
 
 EXPORTED = ["sigattn_fwd", "sigattn_bwd", "sigattn_bwd_workspace_bytes", "sigattn_mask_to_seqlens",
-            "sigattn_valid_flops", "sigattn_worklist_host", "sigattn_last_error", "sigattn_version"]
+            "sigattn_valid_flops", "sigattn_worklist_host", "sigattn_last_error", "sigattn_version",
+            "sigattn_launch_count", "sigattn_set_profile_events"]
 
 
 class SigattnParams(ctypes.Structure):
@@ -68,6 +69,9 @@ def load():
     lib.sigattn_worklist_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           vp, vp, vp, ctypes.c_int64]
     lib.sigattn_worklist_host.restype = ctypes.c_int64
+    lib.sigattn_launch_count.restype = ctypes.c_int64
+    lib.sigattn_set_profile_events.argtypes = [vp, vp, vp, vp]
+    lib.sigattn_set_profile_events.restype = None
     lib.sigattn_last_error.restype = ctypes.c_char_p
     lib.sigattn_version.restype = ctypes.c_char_p
     _lib = lib

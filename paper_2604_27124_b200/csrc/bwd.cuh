@@ -2,28 +2,33 @@
 //
 // The paper splits the backward into a dQ kernel (Alg. 2) and a dK/dV kernel
 // (Alg. 3), each recomputing sigma.  Here the two are fused into ONE key-tile-owned
-// pass: every (b, h, key tile) item keeps K_j, V_j resident and loops
-// over the valid query tiles i, recomputing
-//     S^T  = K_j Q_i^T,   dP^T = V_j dO_i^T                    (Alg. 3)
-//     P^T  = mask . sigma(alpha S^T + b)
-//     dS^T = alpha . P^T (1 - P^T) dP^T                         (alpha of P:669/P:727 folded in)
-//     dV_j += P^T dO_i,  dK_j += dS^T Q_i  -- on chip, atomic-free
-//     dQ_i += dS K_j  -- fp32 partial per key tile,
-//                                                                 reduce-added into a workspace
-// so sigma is evaluated once per element and the tensor work is the credited 10 d per pair.
+// pass: every (b, h, key tile) item keeps K_j, V_j resident and loops over
+// the valid 128-query tiles i, each processed as two 64-query halves q in {0, 1}:
+//     S^T_q  = K_j Q_iq^T,   dP^T_q = V_j dO_iq^T                (Alg. 3)
+//     P^T_q  = mask . sigma(alpha S^T_q + b)
+//     dS^T_q = P^T_q (1 - P^T_q) dP^T_q
+//     dV_j  += P^T_q dO_iq,   dK_j += dS^T_q Q_iq  on chip, atomic-free
+//     dQ_i  += dS_i K_j  (both halves, M = 128)  fp32 partial per key tile
+// alpha is applied once in the epilogues.  sigma is evaluated once per element and
+// the tensor work is the credited 10 d per (query, key) pair.
 //
-// CTA roles (512 threads, persistent):
-//   warp 0      TMA: K_j, V_j (2 slots), Q_i + dO_i ring (kQStages)
-//   warp 1      MMA issuer (one thread)
+// CTA roles (512 threads, persistent, one CTA per SM):
+//   warp 0      TMA: K_j, V_j (2 slots), Q_i + dO_i (2 stages)
+//   warp 1      MMA issuer (one thread); issue order per tile i (look-ahead one tile):
+//                 dV/dK(i, q0) | S,dP(i+1, q0) | dV/dK(i, q1) | dQ(i) | S,dP(i+1, q1)
+//               so warpgroup q0 computes tile i+1 while warpgroup q1 still computes tile i.
 //   warp 2      TMEM allocator
-//   warps 4-11  two compute warpgroups; thread = key row (TMEM lane), WG g = query columns [64g, 64g+64)
-//   warps 12-15 dQ reducer: tcgen05.ld dQ_i (thread = query row) -> red.global.add.v4.f32
-// TMEM (d = 64): S^T [0,128) | dP^T [128,256) | dV [256,320) | dK [320,384) | dQ [384,448).
-// P^T / dS^T (16-bit) are written back over the first half of each WG's own S^T / dP^T columns
-// and feed the dV / dK MMAs straight from TMEM; dS^T is also written to shared memory (128B
-// swizzled, keys as rows) where the same bytes serve as the MN-major A operand of dQ = dS K.
+//   warps 4-7   compute warpgroup for query half 0; warps 8-11 for half 1 (thread = key row)
+//   warps 12-15 epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
+//               dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
+// TMEM (d = 64): S^T_q0 [0,64) S^T_q1 [64,128) dP^T_q0 [128,192) dP^T_q1 [192,256)
+//                dV [256,320) dK [320,384) dQ [384,448).
+// P^T / dS^T (16-bit) are written back over the first half of their own S^T / dP^T columns and
+// feed the dV / dK MMAs from TMEM; dS^T also goes to shared memory (128B-swizzled, keys as rows,
+// double-buffered) where the same bytes are the MN-major A operand of dQ = dS K.
 #pragma once
 #include "fwd.cuh"
+#include "sigmoid.cuh"
 
 namespace sigattn {
 
@@ -36,7 +41,7 @@ struct BwdArgs {
   float bias;
   float scale;
   int B, H, Nq, Nk;
-  float* dq_acc;          // fp32 [B,H,Nq,D], zero on valid rows at entry
+  float* dq_acc;          // fp32 [B,H,Nq,D], zero on valid rows at entry; receives alpha dS K
   void* dk;               // [B,H,Nk,D]
   void* dv;
 };
@@ -44,15 +49,15 @@ struct BwdArgs {
 template <int D>
 struct BwdCfg {
   static_assert(D == 64, "fused backward: d = 64 TMEM plan");
-  static constexpr int kQStages = 2;
   static constexpr int kTileBytes = kTile * D * 2;           // 16 KB
   static constexpr int kKOff = 0;                            // K[2]
   static constexpr int kVOff = kKOff + 2 * kTileBytes;       // V[2]
-  static constexpr int kQOff = kVOff + 2 * kTileBytes;       // Q[kQStages]
-  static constexpr int kDOOff = kQOff + kQStages * kTileBytes;
-  static constexpr int kDSOff = kDOOff + kQStages * kTileBytes;  // dS^T: 2 halves of [128 keys][64 q]
-  static constexpr int kBarOff = kDSOff + 2 * kTile * 128;
-  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 1 + 1 + 1 + 1 + 1 + 1 + 1;
+  static constexpr int kQOff = kVOff + 2 * kTileBytes;       // Q[2]
+  static constexpr int kDOOff = kQOff + 2 * kTileBytes;      // dO[2]
+  static constexpr int kDSOff = kDOOff + 2 * kTileBytes;     // dS^T[2]: 2 halves of [128 keys][64 q]
+  static constexpr int kDSBytes = 2 * kTile * 128;
+  static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
+  static constexpr int kNumBars = 2 + 2 + 2 + 2 + 2 + 2 + 2 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kThreads = 512;
   static constexpr uint32_t kTmemCols = 512;
@@ -63,6 +68,34 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
 }
+
+// Walks this CTA's non-empty work items (static stride) and their query tiles.
+struct TileIter {
+  int it, step, n_items, i, nqt;
+  uint32_t item_c;   // index of the current item among this CTA's non-empty items
+  bool valid;
+  __device__ __forceinline__ void seek(const int4* items) {
+    while (it < n_items && items[it].w <= 0) it += step;
+    valid = it < n_items;
+    nqt = valid ? items[it].w : 0;
+  }
+  __device__ __forceinline__ void init(const int4* items, int n) {
+    it = blockIdx.x;
+    step = gridDim.x;
+    n_items = n;
+    i = 0;
+    item_c = 0;
+    seek(items);
+  }
+  __device__ __forceinline__ void advance(const int4* items) {
+    if (++i >= nqt) {
+      i = 0;
+      it += step;
+      ++item_c;
+      seek(items);
+    }
+  }
+};
 
 template <int D, bool kBf16>
 __global__ void __launch_bounds__(512, 1)
@@ -75,15 +108,15 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* kv_full = bars + 0;        // [2]
   uint64_t* kv_empty = bars + 2;       // [2]
-  uint64_t* qdo_full = bars + 4;       // [kQStages]
-  uint64_t* qdo_empty = qdo_full + C::kQStages;
-  uint64_t* s_full = qdo_empty + C::kQStages;
-  uint64_t* p_full = s_full + 1;
-  uint64_t* ds_free = p_full + 1;
-  uint64_t* dq_full = ds_free + 1;
-  uint64_t* dq_empty = dq_full + 1;
-  uint64_t* acc_full = dq_empty + 1;
-  uint64_t* acc_empty = acc_full + 1;
+  uint64_t* qdo_full = bars + 4;       // [2]
+  uint64_t* qdo_empty = bars + 6;      // [2]
+  uint64_t* s_full = bars + 8;         // [2] per query half
+  uint64_t* p_full = bars + 10;        // [2] per query half
+  uint64_t* ds_free = bars + 12;       // [2] per dS buffer
+  uint64_t* dq_full = bars + 14;
+  uint64_t* dq_empty = bars + 15;
+  uint64_t* acc_full = bars + 16;
+  uint64_t* acc_empty = bars + 17;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -93,18 +126,16 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < C::kQStages; ++i) {
       sm100::mbar_init(&qdo_full[i], 1);
       sm100::mbar_init(&qdo_empty[i], 1);
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&p_full[i], 4);
+      sm100::mbar_init(&ds_free[i], 1);
     }
-    sm100::mbar_init(s_full, 1);
-    sm100::mbar_init(p_full, 8);
-    sm100::mbar_init(ds_free, 1);
     sm100::mbar_init(dq_full, 1);
     sm100::mbar_init(dq_empty, 4);
     sm100::mbar_init(acc_full, 1);
-    sm100::mbar_init(acc_empty, 8);
+    sm100::mbar_init(acc_empty, 4);
     sm100::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -125,7 +156,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     if (lane == 0) {
       const uint64_t pol_kv = sm100::policy_evict_first();
       const uint64_t pol_q = sm100::policy_evict_last();
-      uint32_t kv_c = 0, qi = 0;
+      uint32_t kv_c = 0, t = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int4 item = args.items[it];
         const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
@@ -136,9 +167,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::mbar_arrive_expect_tx(&kv_full[kvb], 2 * C::kTileBytes);
         sm100::tma_load_3d(smem + C::kKOff + kvb * C::kTileBytes, &tmK, &kv_full[kvb], 0, kt * kTile, zh, pol_kv);
         sm100::tma_load_3d(smem + C::kVOff + kvb * C::kTileBytes, &tmV, &kv_full[kvb], 0, kt * kTile, zh, pol_kv);
-        for (int i = 0; i < nqt; ++i, ++qi) {
-          const uint32_t st = qi % C::kQStages;
-          sm100::mbar_wait(&qdo_empty[st], ((qi / C::kQStages) & 1) ^ 1);
+        for (int i = 0; i < nqt; ++i, ++t) {
+          const uint32_t st = t & 1;
+          sm100::mbar_wait(&qdo_empty[st], ((t >> 1) & 1) ^ 1);
           sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kTileBytes);
           sm100::tma_load_3d(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q);
           sm100::tma_load_3d(smem + C::kDOOff + st * C::kTileBytes, &tmDO, &qdo_full[st], 0, i * kTile, zh, pol_q);
@@ -149,7 +180,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
-      constexpr uint32_t idesc_st = sm100::make_idesc_f16(kBf16, 128, 128, false, false);  // S^T, dP^T
+      constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 64, false, false);    // S^T_q, dP^T_q
       constexpr uint32_t idesc_acc = sm100::make_idesc_f16(kBf16, 128, D, false, true);    // dV, dK (A tmem)
       constexpr uint32_t idesc_dq = sm100::make_idesc_f16(kBf16, 128, D, true, true);      // dQ (A = dS MN-major)
       const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
@@ -157,94 +188,117 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
       const uint32_t do_base = sm100::smem_u32(smem + C::kDOOff);
       const uint32_t ds_base = sm100::smem_u32(smem + C::kDSOff);
-      uint32_t kv_c = 0, qi = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int nqt = args.items[it].w;
-        if (nqt <= 0) continue;
-        const uint32_t kvb = kv_c & 1;
-        sm100::mbar_wait(&kv_full[kvb], (kv_c >> 1) & 1);
+
+      // S^T_q = K Q_q^T and dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; both K-major)
+      auto mma1 = [&](uint32_t kvb, uint32_t st, uint32_t q) {
+        const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
+        const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          sm100::mma_ss(tmem + C::kColS + q * 64, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024),
+                        sm100::make_sdesc_sw128(qa + kk * 32, 16, 1024), idesc_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          sm100::mma_ss(tmem + C::kColDP + q * 64, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024),
+                        sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_s, kk > 0);
+        sm100::mma_commit(&s_full[q]);
+      };
+      // dV += P^T_q dO_q ; dK += dS^T_q Q_q   (M = keys, N = d, K = 64 queries; A from TMEM, B MN-major)
+      auto mma2 = [&](uint32_t st, uint32_t q, bool first) {
+        const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + q * 64 + kk * 8,
+                        sm100::make_sdesc_sw128(da + kk * 2048, kTile * 128, 1024), idesc_acc,
+                        (first && kk == 0) ? 0u : 1u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + q * 64 + kk * 8,
+                        sm100::make_sdesc_sw128(qa + kk * 2048, kTile * 128, 1024), idesc_acc,
+                        (first && kk == 0) ? 0u : 1u);
+      };
+      // dQ_i = dS K_j   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major smem, B = K MN-major smem)
+      auto mma_dq = [&](uint32_t kvb, uint32_t buf) {
         const uint32_t ka = k_base + kvb * C::kTileBytes;
-        const uint32_t va = v_base + kvb * C::kTileBytes;
-        for (int i = 0; i < nqt; ++i, ++qi) {
-          const uint32_t st = qi % C::kQStages;
-          sm100::mbar_wait(&qdo_full[st], (qi / C::kQStages) & 1);
+        const uint32_t dsa = ds_base + buf * C::kDSBytes;
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          sm100::mma_ss(tmem + C::kColDQ, sm100::make_sdesc_sw128(dsa + kk * 2048, kTile * 128, 1024),
+                        sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024), idesc_dq, kk > 0);
+      };
+
+      TileIter cur;
+      cur.init(args.items, n_items);
+      if (cur.valid) {
+        sm100::mbar_wait(&kv_full[cur.item_c & 1], (cur.item_c >> 1) & 1);
+        sm100::mbar_wait(&qdo_full[0], 0);
+        sm100::tc_fence_after();
+        mma1(cur.item_c & 1, 0, 0);
+        mma1(cur.item_c & 1, 0, 1);
+      }
+      uint32_t t = 0;
+      while (cur.valid) {
+        TileIter nxt = cur;
+        nxt.advance(args.items);
+        const uint32_t st = t & 1, kvb = cur.item_c & 1;
+        sm100::mbar_wait(&p_full[0], t & 1);
+        if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);
+        sm100::tc_fence_after();
+        mma2(st, 0, cur.i == 0);
+        if (nxt.valid) {
+          if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
+          sm100::mbar_wait(&qdo_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
           sm100::tc_fence_after();
-          const uint32_t qa = q_base + st * C::kTileBytes;
-          const uint32_t da = do_base + st * C::kTileBytes;
-          // S^T = K Q^T  and  dP^T = V dO^T   (M = keys, N = queries, K = d; all K-major)
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            sm100::mma_ss(tmem + C::kColS, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024),
-                          sm100::make_sdesc_sw128(qa + kk * 32, 16, 1024), idesc_st, kk > 0);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            sm100::mma_ss(tmem + C::kColDP, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024),
-                          sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_st, kk > 0);
-          sm100::mma_commit(s_full);
-          sm100::mbar_wait(p_full, qi & 1);
-          if (i == 0) sm100::mbar_wait(acc_empty, (kv_c & 1) ^ 1);
-          sm100::tc_fence_after();
-          // dV += P^T dO ;  dK += dS^T Q   (M = keys, N = d, K = queries; A from TMEM, B MN-major)
-#pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk) {
-            const uint32_t a_off = (kk >> 2) * 64 + (kk & 3) * 8;
-            sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + a_off,
-                          sm100::make_sdesc_sw128(da + kk * 2048, kTile * 128, 1024), idesc_acc,
-                          (i > 0 || kk > 0) ? 1u : 0u);
-          }
-#pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk) {
-            const uint32_t a_off = (kk >> 2) * 64 + (kk & 3) * 8;
-            sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + a_off,
-                          sm100::make_sdesc_sw128(qa + kk * 2048, kTile * 128, 1024), idesc_acc,
-                          (i > 0 || kk > 0) ? 1u : 0u);
-          }
-          // dQ_i = dS K_j   (M = queries, N = d, K = keys; A = dS MN-major smem, B = K MN-major smem)
-          sm100::mbar_wait(dq_empty, (qi & 1) ^ 1);
-          sm100::tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk)
-            sm100::mma_ss(tmem + C::kColDQ, sm100::make_sdesc_sw128(ds_base + kk * 2048, kTile * 128, 1024),
-                          sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024), idesc_dq, kk > 0);
-          sm100::mma_commit(&qdo_empty[st]);
-          sm100::mma_commit(ds_free);
-          sm100::mma_commit(dq_full);
+          mma1(nxt.item_c & 1, (t + 1) & 1, 0);
         }
-        sm100::mma_commit(&kv_empty[kvb]);
-        sm100::mma_commit(acc_full);
-        ++kv_c;
+        sm100::mbar_wait(&p_full[1], t & 1);
+        sm100::tc_fence_after();
+        mma2(st, 1, false);
+        sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
+        sm100::tc_fence_after();
+        mma_dq(kvb, st);
+        sm100::mma_commit(&qdo_empty[st]);
+        sm100::mma_commit(&ds_free[st]);
+        sm100::mma_commit(dq_full);
+        if (cur.i == cur.nqt - 1) {
+          sm100::mma_commit(&kv_empty[kvb]);
+          sm100::mma_commit(acc_full);
+        }
+        if (nxt.valid) mma1(nxt.item_c & 1, (t + 1) & 1, 1);
+        cur = nxt;
+        ++t;
       }
     }
   } else if (warp >= 4 && warp < 12) {
-    // ===================== compute warpgroups =====================
-    const uint32_t g = (warp - 4) >> 2;
+    // ===================== compute warpgroups (query half qh) =====================
+    const uint32_t qh = (warp - 4) >> 2;
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
-    uint8_t* ds_row = smem + C::kDSOff + g * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128;
-    uint32_t kv_c = 0, qi = 0;
+    const uint32_t s_col = C::kColS + qh * 64, dp_col = C::kColDP + qh * 64;
+    uint8_t* ds_row = smem + C::kDSOff + qh * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128;
+    uint32_t t = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
-      const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
+      const int b = item.x, kt = item.z, nqt = item.w;
       if (nqt <= 0) continue;
       const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const float bias = args.bias_per_seq ? args.bias_per_seq[b] : args.bias;
       const float a2 = -args.scale * kLog2e;
       const float b2 = -bias * kLog2e;
-      const float alpha = args.scale;
-      const int key = kt * kTile + (int)row;
-      const bool key_valid = key < nk;
-      for (int i = 0; i < nqt; ++i, ++qi) {
-        sm100::mbar_wait(s_full, qi & 1);
-        sm100::mbar_wait(ds_free, (qi & 1) ^ 1);
+      const bool key_valid = kt * kTile + (int)row < nk;
+      for (int i = 0; i < nqt; ++i, ++t) {
+        sm100::mbar_wait(&s_full[qh], t & 1);
+        sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
-        const int q0 = i * kTile + (int)g * 64;
+        uint8_t* dsr = ds_row + (t & 1) * C::kDSBytes;
+        const int q0 = i * kTile + (int)qh * 64;
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           uint32_t s[32], dp[32];
-          sm100::tmem_ld32(tmem + lane_addr + C::kColS + g * 64 + ch * 32, s);
-          sm100::tmem_ld32(tmem + lane_addr + C::kColDP + g * 64 + ch * 32, dp);
+          sm100::tmem_ld32(tmem + lane_addr + s_col + ch * 32, s);
+          sm100::tmem_ld32(tmem + lane_addr + dp_col + ch * 32, dp);
           sm100::tmem_wait_ld_dep(s);
           sm100::tmem_wait_ld_dep(dp);
           const int qc = q0 + ch * 32;
@@ -252,10 +306,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           uint32_t pp[16], dd[16];
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            float p0 = sm100::rcp_approx(1.0f + sm100::ex2_approx(fmaf(__uint_as_float(s[e]), a2, b2)));
-            float p1 = sm100::rcp_approx(1.0f + sm100::ex2_approx(fmaf(__uint_as_float(s[e + 1]), a2, b2)));
-            float d0 = (p0 - p0 * p0) * __uint_as_float(dp[e]) * alpha;
-            float d1 = (p1 - p1 * p1) * __uint_as_float(dp[e + 1]) * alpha;
+            float p0, p1, u0, u1, d0, d1;
+            sigma2(__uint_as_float(s[e]), __uint_as_float(s[e + 1]), a2, b2, p0, p1);
+            ffma2(u0, u1, p0, p1, -p0, -p1, p0, p1);                   // p (1 - p)
+            fmul2(d0, d1, u0, u1, __uint_as_float(dp[e]), __uint_as_float(dp[e + 1]));
             if (need_mask) {
               const bool v0 = key_valid && (qc + e < nq);
               const bool v1 = key_valid && (qc + e + 1 < nq);
@@ -267,70 +321,37 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             pp[e >> 1] = sm100::pack2<kBf16>(p0, p1);
             dd[e >> 1] = sm100::pack2<kBf16>(d0, d1);
           }
-          sm100::tmem_st16(tmem + lane_addr + C::kColS + g * 64 + ch * 16, pp);
-          sm100::tmem_st16(tmem + lane_addr + C::kColDP + g * 64 + ch * 16, dd);
-          // dS^T row into the swizzled smem tile: 32 queries = 64 B = 16-byte chunks 4ch..4ch+3
+          sm100::tmem_st16(tmem + lane_addr + s_col + ch * 16, pp);
+          sm100::tmem_st16(tmem + lane_addr + dp_col + ch * 16, dd);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint32_t chunk = (uint32_t)(ch * 4 + u) ^ (row & 7);
-            *reinterpret_cast<uint4*>(ds_row + chunk * 16) =
-                make_uint4(dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+            *reinterpret_cast<uint4*>(dsr + chunk * 16) = make_uint4(dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
           }
         }
         sm100::tmem_wait_st();
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(p_full);
+        if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
       }
-      // ---- epilogue: dV, dK rows of this key tile, columns [g*D/2, g*D/2 + D/2)
-      sm100::mbar_wait(acc_full, kv_c & 1);
-      sm100::tc_fence_after();
-      constexpr int kHalf = D / 2;
-      uint32_t rv[32], rk[32];
-      static_assert(kHalf == 32, "d = 64");
-      sm100::tmem_ld32(tmem + lane_addr + C::kColDV + g * kHalf, rv);
-      sm100::tmem_ld32(tmem + lane_addr + C::kColDK + g * kHalf, rk);
-      sm100::tmem_wait_ld_dep(rv);
-      sm100::tmem_wait_ld_dep(rk);
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(acc_empty);
-      if (key < args.Nk) {
-        const size_t off = ((size_t)(b * args.H + h) * args.Nk + key) * D + g * kHalf;
-        uint4* dvp = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.dv) + off);
-        uint4* dkp = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.dk) + off);
-#pragma unroll
-        for (int e = 0; e < kHalf; e += 8) {
-          uint4 wv, wk;
-          wv.x = key_valid ? sm100::pack2<kBf16>(__uint_as_float(rv[e]), __uint_as_float(rv[e + 1])) : 0u;
-          wv.y = key_valid ? sm100::pack2<kBf16>(__uint_as_float(rv[e + 2]), __uint_as_float(rv[e + 3])) : 0u;
-          wv.z = key_valid ? sm100::pack2<kBf16>(__uint_as_float(rv[e + 4]), __uint_as_float(rv[e + 5])) : 0u;
-          wv.w = key_valid ? sm100::pack2<kBf16>(__uint_as_float(rv[e + 6]), __uint_as_float(rv[e + 7])) : 0u;
-          wk.x = key_valid ? sm100::pack2<kBf16>(__uint_as_float(rk[e]), __uint_as_float(rk[e + 1])) : 0u;
-          wk.y = key_valid ? sm100::pack2<kBf16>(__uint_as_float(rk[e + 2]), __uint_as_float(rk[e + 3])) : 0u;
-          wk.z = key_valid ? sm100::pack2<kBf16>(__uint_as_float(rk[e + 4]), __uint_as_float(rk[e + 5])) : 0u;
-          wk.w = key_valid ? sm100::pack2<kBf16>(__uint_as_float(rk[e + 6]), __uint_as_float(rk[e + 7])) : 0u;
-          dvp[e >> 3] = wv;
-          dkp[e >> 3] = wk;
-        }
-      }
-      ++kv_c;
     }
   } else if (warp >= 12) {
-    // ===================== dQ reducer =====================
+    // ===================== epilogue warpgroup: dQ drain + dK/dV =====================
     const uint32_t quarter = warp & 3;
-    const uint32_t row = quarter * 32 + lane;      // query row within the tile
+    const uint32_t row = quarter * 32 + lane;
     const uint32_t lane_addr = (quarter * 32) << 16;
-    uint32_t qi = 0;
+    const float alpha = args.scale;
+    uint32_t t = 0, item_c = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
-      const int b = item.x, h = item.y, nqt = item.w;
+      const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
       if (nqt <= 0) continue;
       const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
-      const size_t zrow0 = (size_t)(b * args.H + h) * args.Nq;
-      for (int i = 0; i < nqt; ++i, ++qi) {
-        sm100::mbar_wait(dq_full, qi & 1);
+      const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
+      const size_t zh = (size_t)(b * args.H + h);
+      for (int i = 0; i < nqt; ++i, ++t) {
+        sm100::mbar_wait(dq_full, t & 1);
         sm100::tc_fence_after();
         uint32_t r0[32], r1[32];
         sm100::tmem_ld32(tmem + lane_addr + C::kColDQ, r0);
@@ -342,17 +363,60 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (lane == 0) sm100::mbar_arrive(dq_empty);
         const int q = i * kTile + (int)row;
         if (q < nq) {
-          float* dst = args.dq_acc + (zrow0 + q) * D;
+          float* dst = args.dq_acc + (zh * args.Nq + q) * D;
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
-            red_add_v4(dst + e, __uint_as_float(r0[e]), __uint_as_float(r0[e + 1]), __uint_as_float(r0[e + 2]),
-                       __uint_as_float(r0[e + 3]));
+            red_add_v4(dst + e, alpha * __uint_as_float(r0[e]), alpha * __uint_as_float(r0[e + 1]),
+                       alpha * __uint_as_float(r0[e + 2]), alpha * __uint_as_float(r0[e + 3]));
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
-            red_add_v4(dst + 32 + e, __uint_as_float(r1[e]), __uint_as_float(r1[e + 1]), __uint_as_float(r1[e + 2]),
-                       __uint_as_float(r1[e + 3]));
+            red_add_v4(dst + 32 + e, alpha * __uint_as_float(r1[e]), alpha * __uint_as_float(r1[e + 1]),
+                       alpha * __uint_as_float(r1[e + 2]), alpha * __uint_as_float(r1[e + 3]));
         }
       }
+      // ---- dV, dK rows of this key tile (dK scaled by alpha)
+      sm100::mbar_wait(acc_full, item_c & 1);
+      sm100::tc_fence_after();
+      const int key = kt * kTile + (int)row;
+      const bool key_valid = key < nk;
+      const size_t off = (zh * args.Nk + key) * D;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        uint32_t r0[32], r1[32];
+        const uint32_t col = which == 0 ? C::kColDV : C::kColDK;
+        const float sc = which == 0 ? 1.0f : alpha;
+        sm100::tmem_ld32(tmem + lane_addr + col, r0);
+        sm100::tmem_ld32(tmem + lane_addr + col + 32, r1);
+        sm100::tmem_wait_ld_dep(r0);
+        sm100::tmem_wait_ld_dep(r1);
+        if (which == 1) {
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(acc_empty);
+        }
+        if (key < args.Nk) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(which == 0 ? args.dv : args.dk) + off);
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 w;
+            w.x = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r0[e]), sc * __uint_as_float(r0[e + 1])) : 0u;
+            w.y = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r0[e + 2]), sc * __uint_as_float(r0[e + 3])) : 0u;
+            w.z = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r0[e + 4]), sc * __uint_as_float(r0[e + 5])) : 0u;
+            w.w = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r0[e + 6]), sc * __uint_as_float(r0[e + 7])) : 0u;
+            dst[e >> 3] = w;
+          }
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 w;
+            w.x = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r1[e]), sc * __uint_as_float(r1[e + 1])) : 0u;
+            w.y = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r1[e + 2]), sc * __uint_as_float(r1[e + 3])) : 0u;
+            w.z = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r1[e + 4]), sc * __uint_as_float(r1[e + 5])) : 0u;
+            w.w = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r1[e + 6]), sc * __uint_as_float(r1[e + 7])) : 0u;
+            dst[4 + (e >> 3)] = w;
+          }
+        }
+      }
+      ++item_c;
     }
   }
 

@@ -15,6 +15,7 @@
 // by sched.cuh from the device seqlens, so fully padded query tiles are never visited
 // and the key loop stops at ceil(n_k / 128) tiles.
 #pragma once
+#include "sigmoid.cuh"
 #include "sm100.cuh"
 
 namespace sigattn {
@@ -229,8 +230,8 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            float p0 = sm100::rcp_approx(1.0f + sm100::ex2_approx(fmaf(__uint_as_float(r[e]), a2, b2)));
-            float p1 = sm100::rcp_approx(1.0f + sm100::ex2_approx(fmaf(__uint_as_float(r[e + 1]), a2, b2)));
+            float p0, p1;
+            sigma2(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), a2, b2, p0, p1);
             if (need_mask) {
               const int kidx = key0 + ch * 32 + e;
               p0 = (kidx < nk) ? p0 : 0.0f;

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -21,6 +22,14 @@ using namespace sigattn;
 namespace {
 
 thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+thread_local cudaEvent_t g_prof[4] = {nullptr, nullptr, nullptr, nullptr};
+
+void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void prof_record(int idx, cudaStream_t s) {
+  if (g_prof[idx]) cudaEventRecord(g_prof[idx], s);
+}
 
 sigattn_status fail(sigattn_status s, const std::string& msg) {
   g_err = msg;
@@ -110,6 +119,7 @@ sigattn_status launch_worklist(int kind, const sigattn_params* p, int4* items, i
   }
   build_worklist_kernel<<<1, kSchedThreads, smem, s>>>(kind, p->B, p->H, p->Nq, p->Nk, p->seqlens_q, p->seqlens_k,
                                                         items, n_items);
+  count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
 }
@@ -118,6 +128,7 @@ sigattn_status launch_zero_rows(void* out, int row_bytes, const sigattn_params* 
                                 const int32_t* gate, int gate_N, int mode, cudaStream_t s) {
   dim3 grid(std::max(1, std::min(64, cdiv((long long)N * row_bytes / 16, 256))), p->B * p->H);
   zero_rows_kernel<<<grid, 256, 0, s>>>(out, row_bytes, p->B, p->H, N, lens, gate, gate_N, mode);
+  count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
 }
@@ -149,7 +160,10 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   auto kern = sigattn_fwd_kernel<D, kBf16, kF32>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
+  prof_record(0, s);
   kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, a);
+  prof_record(1, s);
+  count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
 }
@@ -185,7 +199,10 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   auto kern = sigattn_bwd_kernel<D, kBf16>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
+  prof_record(2, s);
   kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
+  prof_record(3, s);
+  count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
 }
@@ -197,6 +214,15 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 extern "C" {
 
 const char* sigattn_last_error(void) { return g_err.c_str(); }
+
+int64_t sigattn_launch_count(void) { return g_launches.load(); }
+
+void sigattn_set_profile_events(void* fwd_start, void* fwd_stop, void* bwd_start, void* bwd_stop) {
+  g_prof[0] = reinterpret_cast<cudaEvent_t>(fwd_start);
+  g_prof[1] = reinterpret_cast<cudaEvent_t>(fwd_stop);
+  g_prof[2] = reinterpret_cast<cudaEvent_t>(bwd_start);
+  g_prof[3] = reinterpret_cast<cudaEvent_t>(bwd_stop);
+}
 
 const char* sigattn_version(void) { return "sigattn-b200 0.1 (sm_100a tcgen05/TMEM/TMA)"; }
 
@@ -329,6 +355,7 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
     else
       dq_finalize_kernel<false><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
                                                      p->seqlens_q, total8);
+    count_launch();
     CUDA_TRY(cudaGetLastError());
   }
   return SIGATTN_OK;
@@ -341,6 +368,7 @@ sigattn_status sigattn_mask_to_seqlens(const uint8_t* key_padding_mask, int B, i
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaMemsetAsync(nonprefix_flag, 0, sizeof(int32_t), s));
   mask_to_seqlens_kernel<<<B, 256, 0, s>>>(key_padding_mask, N, seqlens, nonprefix_flag);
+  count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
 }
