@@ -15,7 +15,7 @@
 // CTA roles (512 threads, persistent, one CTA per SM):
 //   warp 0      TMA: K_j, V_j (2 slots), Q_i + dO_i (2 stages)
 //   warp 1      MMA issuer (one thread); issue order per tile i (look-ahead one tile):
-//                 dV/dK(i, q0) | S,dP(i+1, q0) | dV/dK(i, q1) | dQ(i) | S,dP(i+1, q1)
+//                 dV/dK(i, q0) | S,dP(i+1, q0) | dV/dK(i, q1) | S,dP(i+1, q1) | dQ(i)
 //               so warpgroup q0 computes tile i+1 while warpgroup q1 still computes tile i.
 //   warp 2      TMEM allocator
 //   warps 4-7   compute warpgroup for query half 0; warps 8-11 for half 1 (thread = key row)
@@ -96,6 +96,29 @@ struct TileIter {
     }
   }
 };
+
+
+// One 32-query chunk of a key row: P^T and dS^T = P^T (1 - P^T) dP^T, packed to 16 bits.
+// kMask: columns e >= nvalid (padded queries) or an invalid key row give P = dS = 0.
+template <bool kMask, bool kBf16>
+__device__ __forceinline__ void bwd_row32(const uint32_t (&s)[32], const uint32_t (&dp)[32], uint32_t (&pp)[16],
+                                          uint32_t (&dd)[16], float a2, float b2, int nvalid) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    float p0, p1, u0, u1, d0, d1;
+    sigma2(__uint_as_float(s[e]), __uint_as_float(s[e + 1]), a2, b2, p0, p1);
+    ffma2(u0, u1, p0, p1, -p0, -p1, p0, p1);                   // p (1 - p)
+    fmul2(d0, d1, u0, u1, __uint_as_float(dp[e]), __uint_as_float(dp[e + 1]));
+    if constexpr (kMask) {
+      p0 = (e < nvalid) ? p0 : 0.0f;
+      d0 = (e < nvalid) ? d0 : 0.0f;
+      p1 = (e + 1 < nvalid) ? p1 : 0.0f;
+      d1 = (e + 1 < nvalid) ? d1 : 0.0f;
+    }
+    pp[e >> 1] = sm100::pack2<kBf16>(p0, p1);
+    dd[e >> 1] = sm100::pack2<kBf16>(d0, d1);
+  }
+}
 
 template <int D, bool kBf16>
 __global__ void __launch_bounds__(512, 1)
@@ -254,17 +277,15 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::mbar_wait(&p_full[1], t & 1);
         sm100::tc_fence_after();
         mma2(st, 1, false);
+        if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
+        if (nxt.valid) mma1(nxt.item_c & 1, (t + 1) & 1, 1);     // half 1 of the next tile before dQ
         sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
         sm100::tc_fence_after();
         mma_dq(kvb, st);
         sm100::mma_commit(&qdo_empty[st]);
         sm100::mma_commit(&ds_free[st]);
         sm100::mma_commit(dq_full);
-        if (cur.i == cur.nqt - 1) {
-          sm100::mma_commit(&kv_empty[kvb]);
-          sm100::mma_commit(acc_full);
-        }
-        if (nxt.valid) mma1(nxt.item_c & 1, (t + 1) & 1, 1);
+        if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);
         cur = nxt;
         ++t;
       }
@@ -301,26 +322,11 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::tmem_ld32(tmem + lane_addr + dp_col + ch * 32, dp);
           sm100::tmem_wait_ld_dep(s);
           sm100::tmem_wait_ld_dep(dp);
-          const int qc = q0 + ch * 32;
-          const bool need_mask = !key_valid || (qc + 32 > nq);
+          // valid query columns in this chunk (0 for a padded key row)
+          const int nvalid = key_valid ? nq - (q0 + ch * 32) : 0;
           uint32_t pp[16], dd[16];
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float p0, p1, u0, u1, d0, d1;
-            sigma2(__uint_as_float(s[e]), __uint_as_float(s[e + 1]), a2, b2, p0, p1);
-            ffma2(u0, u1, p0, p1, -p0, -p1, p0, p1);                   // p (1 - p)
-            fmul2(d0, d1, u0, u1, __uint_as_float(dp[e]), __uint_as_float(dp[e + 1]));
-            if (need_mask) {
-              const bool v0 = key_valid && (qc + e < nq);
-              const bool v1 = key_valid && (qc + e + 1 < nq);
-              p0 = v0 ? p0 : 0.0f;
-              d0 = v0 ? d0 : 0.0f;
-              p1 = v1 ? p1 : 0.0f;
-              d1 = v1 ? d1 : 0.0f;
-            }
-            pp[e >> 1] = sm100::pack2<kBf16>(p0, p1);
-            dd[e >> 1] = sm100::pack2<kBf16>(d0, d1);
-          }
+          if (nvalid >= 32) bwd_row32<false, kBf16>(s, dp, pp, dd, a2, b2, nvalid);
+          else bwd_row32<true, kBf16>(s, dp, pp, dd, a2, b2, nvalid);
           sm100::tmem_st16(tmem + lane_addr + s_col + ch * 16, pp);
           sm100::tmem_st16(tmem + lane_addr + dp_col + ch * 16, dd);
 #pragma unroll

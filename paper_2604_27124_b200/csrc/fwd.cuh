@@ -7,10 +7,10 @@
 //   warp 1      MMA issuer (one thread): S = Q K^T  (SS, both K-major)  -> TMEM S[2] (double buffer)
 //                                        O += P V   (TS, P from TMEM, V MN-major) -> TMEM O
 //   warp 2      TMEM allocator
-//   warps 4-11  two sigmoid warpgroups: WG g owns key columns [64g, 64g+64) of every S tile:
+//   warps 4-19  four sigmoid warpgroups: WG g owns key columns [32g, 32g+32) of every S tile:
 //               tcgen05.ld S -> x = alpha s + b -> sigma -> key mask -> bf16 -> tcgen05.st P
 //               (P aliased onto the first half of its own S columns), then the epilogue for
-//               its half of the O columns (padded query rows written as exact 0).
+//               its quarter of the O columns (padded query rows written as exact 0).
 // Work items (b, h, q-tile) come from a device work list sorted longest-first (LPT), built
 // by sched.cuh from the device seqlens, so fully padded query tiles are never visited
 // and the key loop stops at ceil(n_k / 128) tiles.
@@ -46,7 +46,8 @@ struct FwdCfg {
   static constexpr int kBarOff = kVOff + kStages * kTileBytes;
   static constexpr int kNumBars = 2 + 2 + 3 * kStages + 2 + 2 + 2;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;  // + alignment slack
-  static constexpr int kThreads = 384;
+  static constexpr int kNumWG = 4;                          // sigmoid warpgroups
+  static constexpr int kThreads = 128 + 128 * kNumWG;
   static constexpr uint32_t kTmemCols = 512;
   // TMEM columns
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
@@ -54,8 +55,24 @@ struct FwdCfg {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// 32 scores of one row -> 16 packed 16-bit P values; kMask zeroes columns e >= nvalid (padded keys).
+template <bool kMask, bool kBf16>
+__device__ __forceinline__ void sigmoid_row32(const uint32_t (&r)[32], uint32_t (&pk)[16], float a2, float b2,
+                                              int nvalid) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    float p0, p1;
+    sigma2(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), a2, b2, p0, p1);
+    if constexpr (kMask) {
+      p0 = (e < nvalid) ? p0 : 0.0f;
+      p1 = (e + 1 < nvalid) ? p1 : 0.0f;
+    }
+    pk[e >> 1] = sm100::pack2<kBf16>(p0, p1);
+  }
+}
+
 template <int D, bool kBf16, bool kOutF32>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
 sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
   using C = FwdCfg<D>;
@@ -81,7 +98,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&q_full[i], 1);
       sm100::mbar_init(&q_empty[i], 1);
       sm100::mbar_init(&s_full[i], 1);
-      sm100::mbar_init(&p_full[i], 8);   // one arrival per sigmoid warp
+      sm100::mbar_init(&p_full[i], 4 * C::kNumWG);   // one arrival per sigmoid warp
     }
     for (int i = 0; i < C::kStages; ++i) {
       sm100::mbar_init(&k_full[i], 1);
@@ -89,7 +106,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&kv_empty[i], 1);
     }
     sm100::mbar_init(o_full, 1);
-    sm100::mbar_init(o_empty, 8);
+    sm100::mbar_init(o_empty, 4 * C::kNumWG);
     sm100::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -185,8 +202,8 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           const uint32_t p_col = (si & 1) ? C::kColS1 : C::kColS0;
 #pragma unroll
           for (int kk = 0; kk < kTile / 16; ++kk) {
-            // P for keys [16kk, 16kk+16): WG g = kk/4 stored its 64 keys packed at S cols [64g, 64g+32)
-            const uint32_t a_col = p_col + (kk >> 2) * 64 + (kk & 3) * 8;
+            // P for keys [16kk, 16kk+16): WG g = kk/2 stored its 32 keys packed at S cols [32g, 32g+16)
+            const uint32_t a_col = p_col + (kk >> 1) * 32 + (kk & 1) * 8;
             sm100::mma_ts(tmem + C::kColO, tmem + a_col,
                           sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
                           (j > 0 || kk > 0) ? 1u : 0u);
@@ -202,7 +219,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
   } else if (warp >= 4) {
     // ===================== sigmoid warpgroups + epilogue =====================
-    const uint32_t g = (warp - 4) >> 2;          // warpgroup: key columns [64g, 64g+64)
+    const uint32_t g = (warp - 4) >> 2;          // warpgroup: key columns [32g, 32g+32)
     const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t row = quarter * 32 + lane;    // tile row = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
@@ -218,46 +235,31 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const float b2 = -bias * kLog2e;
       for (int j = 0; j < nkt; ++j) {
         const uint32_t si = s_it + j;
-        const uint32_t scol = (si & 1) ? C::kColS1 : C::kColS0;
+        const uint32_t col = ((si & 1) ? C::kColS1 : C::kColS0) + g * 32;
         sm100::mbar_wait(&s_full[si & 1], (si >> 1) & 1);
         sm100::tc_fence_after();
-        const int key0 = j * kTile + (int)g * 64;
-        const bool need_mask = key0 + 64 > nk;
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          uint32_t r[32];
-          sm100::tmem_ld32_sync(tmem + lane_addr + scol + g * 64 + ch * 32, r);
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float p0, p1;
-            sigma2(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), a2, b2, p0, p1);
-            if (need_mask) {
-              const int kidx = key0 + ch * 32 + e;
-              p0 = (kidx < nk) ? p0 : 0.0f;
-              p1 = (kidx + 1 < nk) ? p1 : 0.0f;
-            }
-            pk[e >> 1] = sm100::pack2<kBf16>(p0, p1);
-          }
-          sm100::tmem_st16(tmem + lane_addr + scol + g * 64 + ch * 16, pk);
-        }
+        const int nvalid = nk - (j * kTile + (int)g * 32);   // valid keys in this warpgroup's 32 columns
+        uint32_t r[32], pk[16];
+        sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+        if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, nvalid);
+        else sigmoid_row32<true, kBf16>(r, pk, a2, b2, nvalid);
+        sm100::tmem_st16(tmem + lane_addr + col, pk);
         sm100::tmem_wait_st();
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&p_full[si & 1]);
       }
       s_it += nkt;
-      // ---- epilogue: O rows of this q tile, columns [g*D/2, g*D/2 + D/2)
+      // ---- epilogue: O rows of this q tile, columns [g*D/4, g*D/4 + D/4)
       sm100::mbar_wait(o_full, c & 1);
       sm100::tc_fence_after();
-      constexpr int kHalf = D / 2;
+      constexpr int kHalf = D / C::kNumWG;   // columns per warpgroup
       uint32_t ov[kHalf];
-#pragma unroll
-      for (int cc = 0; cc < kHalf / 32; ++cc) {
-        uint32_t r[32];
-        sm100::tmem_ld32_sync(tmem + lane_addr + C::kColO + g * kHalf + cc * 32, r);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) ov[cc * 32 + e] = r[e];
+      if constexpr (kHalf == 32) {
+        sm100::tmem_ld32_sync(tmem + lane_addr + C::kColO + g * kHalf, ov);
+      } else {
+        static_assert(kHalf == 16, "D / kNumWG");
+        sm100::tmem_ld16_sync(tmem + lane_addr + C::kColO + g * kHalf, ov);
       }
       sm100::tc_fence_before();
       __syncwarp();
