@@ -234,10 +234,13 @@ def main_ours(args):
     if sampler:
         sampler.start()
     n0 = lib.sigattn_launch_count()
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     start.record()
     for i in range(K):
+        marks[i].record()
         lib.sigattn_set_profile_events(*[e.cuda_event for e in ev[i]])
         step()
+    marks[K].record()
     stop.record()
     lib.sigattn_set_profile_events(None, None, None, None)
     torch.cuda.synchronize()
@@ -246,6 +249,12 @@ def main_ours(args):
     if world > 1:
         dist.barrier()
     ms_total = start.elapsed_time(stop)
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(K)]
+    print(f"[bench rank {rank}] per-step ms: " + " ".join(f"{x:.3f}" for x in step_ms), file=sys.stderr)
+    print(f"[bench rank {rank}] fwd kernel ms: " + " ".join(f"{ev[i][0].elapsed_time(ev[i][1]):.3f}" for i in range(K)),
+          file=sys.stderr)
+    print(f"[bench rank {rank}] bwd kernel ms: " + " ".join(f"{ev[i][2].elapsed_time(ev[i][3]):.3f}" for i in range(K)),
+          file=sys.stderr)
     fwd_ms = statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for i in range(K))
     bwd_ms = statistics.mean(ev[i][2].elapsed_time(ev[i][3]) for i in range(K))
     t = torch.tensor([ms_total, fwd_ms, bwd_ms], dtype=torch.float64, device=dev)

@@ -111,6 +111,10 @@ int64_t sigattn_worklist_host(int kind, int B, int H, int Nq, int Nk, const int3
  * call's stream (cudaEvent_t passed as void*).  Pass NULLs to disable.                          */
 int64_t sigattn_launch_count(void);
 void sigattn_set_profile_events(void* fwd_start, void* fwd_stop, void* bwd_start, void* bwd_stop);
+/* Debug builds compiled with -DSIGATTN_TRACE=1 only: device buffer of grid x 4096 int64 that the
+ * kernels fill with clock64() pipeline timestamps (thread-local setting; NULL disables).  A no-op
+ * in release builds.                                                                            */
+void sigattn_set_trace_buffer(void* device_buffer);
 
 const char* sigattn_last_error(void); /* thread-local message of the last failing call */
 const char* sigattn_version(void);

@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "SIGATTN_OK", 1: "SIGATTN_EINVAL", 2: "SIGATTN_EUNSUPPORTED",
 
 EXPORTED = ["sigattn_fwd", "sigattn_bwd", "sigattn_bwd_workspace_bytes", "sigattn_mask_to_seqlens",
             "sigattn_valid_flops", "sigattn_worklist_host", "sigattn_last_error", "sigattn_version",
-            "sigattn_launch_count", "sigattn_set_profile_events"]
+            "sigattn_launch_count", "sigattn_set_profile_events", "sigattn_set_trace_buffer"]
 
 
 class SigattnParams(ctypes.Structure):
@@ -46,10 +46,11 @@ _lib = None
 
 
 def load():
-    """Load libsigattn.so; raises if it has not been built (no fallback)."""
-    global _lib
+    """Load libsigattn.so (or $SIGATTN_LIB, e.g. a trace build); raises if missing (no fallback)."""
+    global _lib, LIB_PATH
     if _lib is not None:
         return _lib
+    LIB_PATH = os.environ.get("SIGATTN_LIB", LIB_PATH)
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} missing: build it with `python -m paper_2604_27124_b200.build` "
                           "or __graft_entry__.build() -- there is no CPU fallback")
@@ -72,6 +73,8 @@ def load():
     lib.sigattn_launch_count.restype = ctypes.c_int64
     lib.sigattn_set_profile_events.argtypes = [vp, vp, vp, vp]
     lib.sigattn_set_profile_events.restype = None
+    lib.sigattn_set_trace_buffer.argtypes = [vp]
+    lib.sigattn_set_trace_buffer.restype = None
     lib.sigattn_last_error.restype = ctypes.c_char_p
     lib.sigattn_version.restype = ctypes.c_char_p
     _lib = lib

@@ -43,6 +43,14 @@ def build(force: bool = False, verbose: bool = False, extra=None) -> str:
     return LIB
 
 
+def build_trace() -> str:
+    """Debug build with -DSIGATTN_TRACE=1 (clock64 pipeline timestamps) -> libsigattn_trace.so."""
+    out = os.path.join(PKG, "libsigattn_trace.so")
+    cmd = [NVCC] + NVCC_FLAGS + ["-DSIGATTN_TRACE=1", os.path.join(CSRC, "sigattn.cu"), "-o", out]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

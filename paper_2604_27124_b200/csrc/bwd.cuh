@@ -12,15 +12,16 @@
 // alpha is applied once in the epilogues.  sigma is evaluated once per element and
 // the tensor work is the credited 10 d per (query, key) pair.
 //
-// CTA roles (512 threads, persistent, one CTA per SM):
-//   warp 0      TMA: K_j, V_j (2 slots), Q_i + dO_i (2 stages)
-//   warp 1      MMA issuer (one thread); issue order per tile i (look-ahead one tile):
+// CTA roles (512 threads, persistent, one CTA per SM; single-thread roles in the highest warp ids,
+// which the warp scheduler favours):
+//   warps 0-3   compute warpgroup for query half 0; warps 4-7 for half 1 (thread = key row)
+//   warps 8-11  epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
+//               dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
+//   warp 12     TMA: K_j, V_j (2 slots), Q_i + dO_i (2 stages)
+//   warp 13     MMA issuer (one elected thread); issue order per tile i (look-ahead one tile):
 //                 dV/dK(i, q0) | S,dP(i+1, q0) | dV/dK(i, q1) | S,dP(i+1, q1) | dQ(i)
 //               so warpgroup q0 computes tile i+1 while warpgroup q1 still computes tile i.
-//   warp 2      TMEM allocator
-//   warps 4-7   compute warpgroup for query half 0; warps 8-11 for half 1 (thread = key row)
-//   warps 12-15 epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
-//               dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
+//   warp 14     TMEM allocator
 // TMEM (d = 64): S^T_q0 [0,64) S^T_q1 [64,128) dP^T_q0 [128,192) dP^T_q1 [192,256)
 //                dV [256,320) dK [320,384) dQ [384,448).
 // P^T / dS^T (16-bit) are written back over the first half of their own S^T / dP^T columns and
@@ -60,6 +61,7 @@ struct BwdCfg {
   static constexpr int kNumBars = 2 + 2 + 2 + 2 + 2 + 2 + 2 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kThreads = 512;
+  static constexpr int kWarpEpi = 8, kWarpTMA = 12, kWarpMMA = 13, kWarpAlloc = 14;
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D, kColDQ = 256 + 2 * D;
 };
@@ -161,48 +163,52 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     sm100::mbar_init(acc_empty, 4);
     sm100::fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == C::kWarpTMA && lane == 0) {
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
     sm100::tma_prefetch_desc(&tmV);
     sm100::tma_prefetch_desc(&tmDO);
   }
-  if (warp == 2) sm100::tmem_alloc<C::kTmemCols>(tmem_holder);
+  if (warp == C::kWarpAlloc) sm100::tmem_alloc<C::kTmemCols>(tmem_holder);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   const int n_items = *args.n_items;
 
-  if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      const uint64_t pol_kv = sm100::policy_evict_first();
-      const uint64_t pol_q = sm100::policy_evict_last();
-      uint32_t kv_c = 0, t = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int4 item = args.items[it];
-        const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
-        if (nqt <= 0) continue;
-        const int zh = b * args.H + h;
-        const uint32_t kvb = kv_c & 1;
-        sm100::mbar_wait(&kv_empty[kvb], ((kv_c >> 1) & 1) ^ 1);
+  if (warp == C::kWarpTMA) {
+    // ===================== TMA producer (whole warp waits, one elected lane issues) =====================
+    const uint64_t pol_kv = sm100::policy_evict_first();
+    const uint64_t pol_q = sm100::policy_evict_last();
+    uint32_t kv_c = 0, t = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
+      if (nqt <= 0) continue;
+      const int zh = b * args.H + h;
+      const uint32_t kvb = kv_c & 1;
+      sm100::mbar_wait(&kv_empty[kvb], ((kv_c >> 1) & 1) ^ 1);
+      if (sm100::elect_one()) {
         sm100::mbar_arrive_expect_tx(&kv_full[kvb], 2 * C::kTileBytes);
         sm100::tma_load_3d(smem + C::kKOff + kvb * C::kTileBytes, &tmK, &kv_full[kvb], 0, kt * kTile, zh, pol_kv);
         sm100::tma_load_3d(smem + C::kVOff + kvb * C::kTileBytes, &tmV, &kv_full[kvb], 0, kt * kTile, zh, pol_kv);
-        for (int i = 0; i < nqt; ++i, ++t) {
-          const uint32_t st = t & 1;
-          sm100::mbar_wait(&qdo_empty[st], ((t >> 1) & 1) ^ 1);
+      }
+      __syncwarp();
+      for (int i = 0; i < nqt; ++i, ++t) {
+        const uint32_t st = t & 1;
+        sm100::mbar_wait(&qdo_empty[st], ((t >> 1) & 1) ^ 1);
+        if (sm100::elect_one()) {
           sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kTileBytes);
           sm100::tma_load_3d(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q);
           sm100::tma_load_3d(smem + C::kDOOff + st * C::kTileBytes, &tmDO, &qdo_full[st], 0, i * kTile, zh, pol_q);
         }
-        ++kv_c;
+        __syncwarp();
       }
+      ++kv_c;
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+  } else if (warp == C::kWarpMMA) {
+    // ===================== MMA issuer (whole warp waits, one elected lane issues) =====================
+    {
       constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 64, false, false);    // S^T_q, dP^T_q
       constexpr uint32_t idesc_acc = sm100::make_idesc_f16(kBf16, 128, D, false, true);    // dV, dK (A tmem)
       constexpr uint32_t idesc_dq = sm100::make_idesc_f16(kBf16, 128, D, true, true);      // dQ (A = dS MN-major)
@@ -256,8 +262,11 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::mbar_wait(&kv_full[cur.item_c & 1], (cur.item_c >> 1) & 1);
         sm100::mbar_wait(&qdo_full[0], 0);
         sm100::tc_fence_after();
-        mma1(cur.item_c & 1, 0, 0);
-        mma1(cur.item_c & 1, 0, 1);
+        if (sm100::elect_one()) {
+          mma1(cur.item_c & 1, 0, 0);
+          mma1(cur.item_c & 1, 0, 1);
+        }
+        __syncwarp();
       }
       uint32_t t = 0;
       while (cur.valid) {
@@ -267,32 +276,40 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::mbar_wait(&p_full[0], t & 1);
         if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);
         sm100::tc_fence_after();
-        mma2(st, 0, cur.i == 0);
+        if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
+        __syncwarp();
         if (nxt.valid) {
           if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
           sm100::mbar_wait(&qdo_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
           sm100::tc_fence_after();
-          mma1(nxt.item_c & 1, (t + 1) & 1, 0);
+          if (sm100::elect_one()) mma1(nxt.item_c & 1, (t + 1) & 1, 0);
+          __syncwarp();
         }
         sm100::mbar_wait(&p_full[1], t & 1);
         sm100::tc_fence_after();
-        mma2(st, 1, false);
-        if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
-        if (nxt.valid) mma1(nxt.item_c & 1, (t + 1) & 1, 1);     // half 1 of the next tile before dQ
+        if (sm100::elect_one()) {
+          mma2(st, 1, false);
+          if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
+          if (nxt.valid) mma1(nxt.item_c & 1, (t + 1) & 1, 1);     // half 1 of the next tile before dQ
+        }
+        __syncwarp();
         sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
         sm100::tc_fence_after();
-        mma_dq(kvb, st);
-        sm100::mma_commit(&qdo_empty[st]);
-        sm100::mma_commit(&ds_free[st]);
-        sm100::mma_commit(dq_full);
-        if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);
+        if (sm100::elect_one()) {
+          mma_dq(kvb, st);
+          sm100::mma_commit(&qdo_empty[st]);
+          sm100::mma_commit(&ds_free[st]);
+          sm100::mma_commit(dq_full);
+          if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);
+        }
+        __syncwarp();
         cur = nxt;
         ++t;
       }
     }
-  } else if (warp >= 4 && warp < 12) {
+  } else if (warp < C::kWarpEpi) {
     // ===================== compute warpgroups (query half qh) =====================
-    const uint32_t qh = (warp - 4) >> 2;
+    const uint32_t qh = warp >> 2;
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
@@ -342,7 +359,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp < C::kWarpTMA) {
     // ===================== epilogue warpgroup: dQ drain + dK/dV =====================
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;
@@ -428,7 +445,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 2) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+  if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);
 }
 
 }  // namespace sigattn

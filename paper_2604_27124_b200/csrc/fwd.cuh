@@ -3,14 +3,14 @@
 //   O[z, M, h, :] = sum over key tiles N < n_k[z] of  sigma(alpha Q_M K_N^T + b_z) masked  . V_N
 //
 // One CTA per SM (persistent), warp-specialised:
-//   warp 0      TMA producer: Q tile (double-buffered) and a K/V ring of kStages tiles
-//   warp 1      MMA issuer (one thread): S = Q K^T  (SS, both K-major)  -> TMEM S[2] (double buffer)
-//                                        O += P V   (TS, P from TMEM, V MN-major) -> TMEM O
-//   warp 2      TMEM allocator
-//   warps 4-19  four sigmoid warpgroups: WG g owns key columns [32g, 32g+32) of every S tile:
+//   warps 0-15  four sigmoid warpgroups: WG g owns key columns [32g, 32g+32) of every S tile:
 //               tcgen05.ld S -> x = alpha s + b -> sigma -> key mask -> bf16 -> tcgen05.st P
 //               (P aliased onto the first half of its own S columns), then the epilogue for
 //               its quarter of the O columns (padded query rows written as exact 0).
+//   warp 16     TMA producer: Q tile (double-buffered) and a K/V ring of kStages tiles
+//   warp 17     MMA issuer (one elected thread): S = Q K^T (SS, both K-major) -> TMEM S[2]
+//                                                O += P V  (TS, P from TMEM, V MN-major) -> TMEM O
+//   warp 18     TMEM allocator
 // Work items (b, h, q-tile) come from a device work list sorted longest-first (LPT), built
 // by sched.cuh from the device seqlens, so fully padded query tiles are never visited
 // and the key loop stops at ceil(n_k / 128) tiles.
@@ -33,6 +33,7 @@ struct FwdArgs {
   float scale;
   int B, H, Nq, Nk;
   void* o;                // bf16/fp16 [B,H,Nq,D] or fp32 partial
+  long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots
 };
 
 template <int D>
@@ -46,8 +47,11 @@ struct FwdCfg {
   static constexpr int kBarOff = kVOff + kStages * kTileBytes;
   static constexpr int kNumBars = 2 + 2 + 3 * kStages + 2 + 2 + 2;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;  // + alignment slack
-  static constexpr int kNumWG = 4;                          // sigmoid warpgroups
-  static constexpr int kThreads = 128 + 128 * kNumWG;
+  static constexpr int kNumWG = 4;                          // sigmoid warpgroups: warps [0, 4 kNumWG)
+  // Single-thread roles sit in the HIGHEST warp ids: the warp scheduler favours high warp ids, so
+  // the MMA / TMA issuers are never starved by the sigmoid warps sharing their sub-partition.
+  static constexpr int kWarpTMA = 4 * kNumWG, kWarpMMA = kWarpTMA + 1, kWarpAlloc = kWarpTMA + 2;
+  static constexpr int kThreads = 32 * (4 * kNumWG + 4);
   static constexpr uint32_t kTmemCols = 512;
   // TMEM columns
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
@@ -109,12 +113,12 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     sm100::mbar_init(o_empty, 4 * C::kNumWG);
     sm100::fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == C::kWarpTMA && lane == 0) {
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
     sm100::tma_prefetch_desc(&tmV);
   }
-  if (warp == 2) sm100::tmem_alloc<C::kTmemCols>(tmem_holder);
+  if (warp == C::kWarpAlloc) sm100::tmem_alloc<C::kTmemCols>(tmem_holder);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -124,27 +128,31 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   const int BH = args.B * args.H;
   (void)BH;
 
-  if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      const uint64_t pol_q = sm100::policy_evict_first();
-      const uint64_t pol_kv = sm100::policy_evict_last();
-      uint32_t kv_it = 0, c = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int4 item = args.items[it];
-        const int b = item.x, h = item.y, qt = item.z, nkt = item.w;
-        if (nkt <= 0) continue;
-        const int zh = b * args.H + h;
-        const uint32_t qb = c & 1, qph = (c >> 1) & 1;
-        sm100::mbar_wait(&q_empty[qb], qph ^ 1);
+  if (warp == C::kWarpTMA) {
+    // ===================== TMA producer (whole warp waits, one elected lane issues) =====================
+    const uint64_t pol_q = sm100::policy_evict_first();
+    const uint64_t pol_kv = sm100::policy_evict_last();
+    uint32_t kv_it = 0, c = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      const int b = item.x, h = item.y, qt = item.z, nkt = item.w;
+      if (nkt <= 0) continue;
+      const int zh = b * args.H + h;
+      const uint32_t qb = c & 1, qph = (c >> 1) & 1;
+      sm100::mbar_wait(&q_empty[qb], qph ^ 1);
+      if (sm100::elect_one()) {
         sm100::mbar_arrive_expect_tx(&q_full[qb], C::kTileBytes);
         uint8_t* qs = smem + C::kQOff + qb * C::kTileBytes;
 #pragma unroll
         for (int s = 0; s < C::kSub; ++s)
           sm100::tma_load_3d(qs + s * (kTile * 128), &tmQ, &q_full[qb], s * 64, qt * kTile, zh, pol_q);
-        for (int j = 0; j < nkt; ++j, ++kv_it) {
-          const uint32_t st = kv_it % C::kStages, ph = (kv_it / C::kStages) & 1;
-          sm100::mbar_wait(&kv_empty[st], ph ^ 1);
+      }
+      __syncwarp();
+      for (int j = 0; j < nkt; ++j, ++kv_it) {
+        const uint32_t st = kv_it % C::kStages, ph = (kv_it / C::kStages) & 1;
+        sm100::mbar_wait(&kv_empty[st], ph ^ 1);
+        if (sm100::elect_one()) {
+          sm100::trace_event(args.trace, kv_it, 512);
           uint8_t* ks = smem + C::kKOff + st * C::kTileBytes;
           uint8_t* vs = smem + C::kVOff + st * C::kTileBytes;
           sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
@@ -156,30 +164,31 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           for (int s = 0; s < C::kSub; ++s)
             sm100::tma_load_3d(vs + s * (kTile * 128), &tmV, &v_full[st], s * 64, j * kTile, zh, pol_kv);
         }
-        ++c;
+        __syncwarp();
       }
+      ++c;
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 128, false, false);
-      constexpr uint32_t idesc_o = sm100::make_idesc_f16(kBf16, 128, D, false, true);
-      const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
-      const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
-      const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
-      uint32_t kv_it = 0, s_it = 0, c = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int nkt = args.items[it].w;
-        if (nkt <= 0) continue;
-        const uint32_t qb = c & 1;
-        sm100::mbar_wait(&q_full[qb], (c >> 1) & 1);
-        const uint32_t qa = q_base + qb * C::kTileBytes;
-        auto issue_s = [&](uint32_t kvi, uint32_t si) {
-          const uint32_t st = kvi % C::kStages;
-          sm100::mbar_wait(&k_full[st], (kvi / C::kStages) & 1);
-          sm100::tc_fence_after();
-          const uint32_t ka = k_base + st * C::kTileBytes;
-          const uint32_t d_s = tmem + ((si & 1) ? C::kColS1 : C::kColS0);
+  } else if (warp == C::kWarpMMA) {
+    // ===================== MMA issuer (whole warp waits, one elected lane issues) =====================
+    constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 128, false, false);
+    constexpr uint32_t idesc_o = sm100::make_idesc_f16(kBf16, 128, D, false, true);
+    const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
+    const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
+    const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
+    uint32_t kv_it = 0, s_it = 0, c = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int nkt = args.items[it].w;
+      if (nkt <= 0) continue;
+      const uint32_t qb = c & 1;
+      sm100::mbar_wait(&q_full[qb], (c >> 1) & 1);
+      const uint32_t qa = q_base + qb * C::kTileBytes;
+      auto issue_s = [&](uint32_t kvi, uint32_t si) {
+        const uint32_t st = kvi % C::kStages;
+        sm100::mbar_wait(&k_full[st], (kvi / C::kStages) & 1);
+        sm100::tc_fence_after();
+        const uint32_t ka = k_base + st * C::kTileBytes;
+        const uint32_t d_s = tmem + ((si & 1) ? C::kColS1 : C::kColS0);
+        if (sm100::elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
@@ -187,19 +196,24 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                           sm100::make_sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
           }
           sm100::mma_commit(&s_full[si & 1]);
-        };
-        issue_s(kv_it, s_it);
-        for (int j = 0; j < nkt; ++j) {
-          if (j + 1 < nkt) issue_s(kv_it + j + 1, s_it + j + 1);
-          const uint32_t si = s_it + j;
-          sm100::mbar_wait(&p_full[si & 1], (si >> 1) & 1);
-          if (j == 0) sm100::mbar_wait(o_empty, (c & 1) ^ 1);   // epilogue drained the previous O
-          const uint32_t kvi = kv_it + j;
-          const uint32_t st = kvi % C::kStages;
-          sm100::mbar_wait(&v_full[st], (kvi / C::kStages) & 1);
-          sm100::tc_fence_after();
-          const uint32_t va = v_base + st * C::kTileBytes;
-          const uint32_t p_col = (si & 1) ? C::kColS1 : C::kColS0;
+          sm100::trace_event(args.trace, 512 + si, 1024);
+        }
+        __syncwarp();
+      };
+      issue_s(kv_it, s_it);
+      for (int j = 0; j < nkt; ++j) {
+        if (j + 1 < nkt) issue_s(kv_it + j + 1, s_it + j + 1);
+        const uint32_t si = s_it + j;
+        sm100::mbar_wait(&p_full[si & 1], (si >> 1) & 1);
+        if (j == 0) sm100::mbar_wait(o_empty, (c & 1) ^ 1);   // epilogue drained the previous O
+        const uint32_t kvi = kv_it + j;
+        const uint32_t st = kvi % C::kStages;
+        sm100::mbar_wait(&v_full[st], (kvi / C::kStages) & 1);
+        sm100::tc_fence_after();
+        const uint32_t va = v_base + st * C::kTileBytes;
+        const uint32_t p_col = (si & 1) ? C::kColS1 : C::kColS0;
+        if (sm100::elect_one()) {
+          sm100::trace_event(args.trace, 1024 + si, 1536);
 #pragma unroll
           for (int kk = 0; kk < kTile / 16; ++kk) {
             // P for keys [16kk, 16kk+16): WG g = kk/2 stored its 32 keys packed at S cols [32g, 32g+16)
@@ -209,17 +223,22 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                           (j > 0 || kk > 0) ? 1u : 0u);
           }
           sm100::mma_commit(&kv_empty[st]);
+          sm100::trace_event(args.trace, 1536 + si, 2048);
         }
+        __syncwarp();
+      }
+      if (sm100::elect_one()) {
         sm100::mma_commit(&q_empty[qb]);
         sm100::mma_commit(o_full);
-        kv_it += nkt;
-        s_it += nkt;
-        ++c;
       }
+      __syncwarp();
+      kv_it += nkt;
+      s_it += nkt;
+      ++c;
     }
-  } else if (warp >= 4) {
+  } else if (warp < C::kWarpTMA) {
     // ===================== sigmoid warpgroups + epilogue =====================
-    const uint32_t g = (warp - 4) >> 2;          // warpgroup: key columns [32g, 32g+32)
+    const uint32_t g = warp >> 2;                // warpgroup: key columns [32g, 32g+32)
     const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t row = quarter * 32 + lane;    // tile row = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
@@ -237,6 +256,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         const uint32_t si = s_it + j;
         const uint32_t col = ((si & 1) ? C::kColS1 : C::kColS0) + g * 32;
         sm100::mbar_wait(&s_full[si & 1], (si >> 1) & 1);
+        if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 2048 + si, 2560);
         sm100::tc_fence_after();
         const int nvalid = nk - (j * kTile + (int)g * 32);   // valid keys in this warpgroup's 32 columns
         uint32_t r[32], pk[16];
@@ -248,6 +268,8 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&p_full[si & 1]);
+        if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 2560 + si, 3072);
+        if (lane == 0 && warp == 4 * C::kNumWG - 1) sm100::trace_event(args.trace, 3072 + si, 3584);
       }
       s_it += nkt;
       // ---- epilogue: O rows of this q tile, columns [g*D/4, g*D/4 + D/4)
@@ -296,7 +318,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 2) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+  if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);
 }
 
 }  // namespace sigattn

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -24,6 +25,7 @@ namespace {
 thread_local std::string g_err;
 std::atomic<long long> g_launches{0};
 thread_local cudaEvent_t g_prof[4] = {nullptr, nullptr, nullptr, nullptr};
+thread_local long long* g_trace = nullptr;
 
 void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
@@ -156,6 +158,7 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   a.Nq = p->Nq;
   a.Nk = p->Nk;
   a.o = o;
+  a.trace = g_trace;
   using C = FwdCfg<D>;
   auto kern = sigattn_fwd_kernel<D, kBf16, kF32>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
@@ -209,6 +212,29 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Small device scratch for the forward work list, cached per (device, stream) so that calls on
+// one stream reuse it in stream order and calls on different streams never share it.  Grows
+// geometrically; a replaced buffer is released with cudaFreeAsync on its own stream (after the
+// work that used it).  This is the only memory the library owns.
+sigattn_status get_scratch(cudaStream_t s, size_t bytes, void** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> cache;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto& e = cache[{dev, s}];
+  if (e.second < bytes) {
+    if (e.first) cudaFreeAsync(e.first, s);
+    size_t nb = std::max(bytes, 2 * e.second);
+    nb = align_up(std::max<size_t>(nb, 1 << 16), 1 << 16);
+    void* p = nullptr;
+    CUDA_TRY(cudaMallocAsync(&p, nb, s));
+    e = {p, nb};
+  }
+  *out = e.first;
+  return SIGATTN_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -216,6 +242,8 @@ extern "C" {
 const char* sigattn_last_error(void) { return g_err.c_str(); }
 
 int64_t sigattn_launch_count(void) { return g_launches.load(); }
+
+void sigattn_set_trace_buffer(void* device_buffer) { g_trace = reinterpret_cast<long long*>(device_buffer); }
 
 void sigattn_set_profile_events(void* fwd_start, void* fwd_stop, void* bwd_start, void* bwd_stop) {
   g_prof[0] = reinterpret_cast<cudaEvent_t>(fwd_start);
@@ -277,10 +305,9 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
   const bool f32 = (p->flags & SIGATTN_F_OUT_F32_PARTIAL) != 0;
   const int elem_out = f32 ? 4 : 2;
   const int max_items = p->B * p->H * cdiv(p->Nq, 128);
-  // stream-ordered scratch for the work list (pool-cached by the CUDA runtime)
   void* scratch = nullptr;
   const size_t bytes = 16 + (size_t)max_items * sizeof(int4);
-  CUDA_TRY(cudaMallocAsync(&scratch, bytes, s));
+  if ((st = get_scratch(s, bytes, &scratch)) != SIGATTN_OK) return st;
   int* n_items = reinterpret_cast<int*>(scratch);
   int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(scratch) + 16);
   st = launch_worklist(0, p, items, n_items, s);
@@ -300,8 +327,6 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
                     : launch_fwd<128, false, false>(p, q, k, v, o, items, n_items, max_items, s);
     }
   }
-  cudaError_t fe = cudaFreeAsync(scratch, s);
-  if (st == SIGATTN_OK && fe != cudaSuccess) return fail(SIGATTN_ECUDA, cudaGetErrorString(fe));
   return st;
 }
 

@@ -10,7 +10,17 @@
 #define SIGATTN_WATCHDOG 1   // trap instead of hanging forever on a lost mbarrier phase
 #endif
 
+#ifndef SIGATTN_TRACE
+#define SIGATTN_TRACE 0   // 1: kernels record clock64() timestamps of pipeline events (debug builds only)
+#endif
+
 namespace sm100 {
+
+__device__ __forceinline__ void trace_event(long long* buf, int slot, int limit) {
+#if SIGATTN_TRACE
+  if (buf && slot < limit) buf[(size_t)blockIdx.x * 4096 + slot] = clock64();
+#endif
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
