@@ -45,6 +45,7 @@ struct BwdArgs {
   float* dq_acc;          // fp32 [B,H,Nq,D], zero on valid rows at entry; receives alpha dS K
   void* dk;               // [B,H,Nk,D]
   void* dv;
+  long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots (8 events x 512 tiles)
 };
 
 template <int D>
@@ -187,7 +188,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       if (nqt <= 0) continue;
       const int zh = b * args.H + h;
       const uint32_t kvb = kv_c & 1;
-      sm100::mbar_wait(&kv_empty[kvb], ((kv_c >> 1) & 1) ^ 1);
+      sm100::mbar_wait_sleep(&kv_empty[kvb], ((kv_c >> 1) & 1) ^ 1);
       if (sm100::elect_one()) {
         sm100::mbar_arrive_expect_tx(&kv_full[kvb], 2 * C::kTileBytes);
         sm100::tma_load_3d(smem + C::kKOff + kvb * C::kTileBytes, &tmK, &kv_full[kvb], 0, kt * kTile, zh, pol_kv);
@@ -196,7 +197,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       __syncwarp();
       for (int i = 0; i < nqt; ++i, ++t) {
         const uint32_t st = t & 1;
-        sm100::mbar_wait(&qdo_empty[st], ((t >> 1) & 1) ^ 1);
+        sm100::mbar_wait_sleep(&qdo_empty[st], ((t >> 1) & 1) ^ 1);
         if (sm100::elect_one()) {
           sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kTileBytes);
           sm100::tma_load_3d(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q);
@@ -274,6 +275,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         nxt.advance(args.items);
         const uint32_t st = t & 1, kvb = cur.item_c & 1;
         sm100::mbar_wait(&p_full[0], t & 1);
+        if (lane == 0) sm100::trace_event(args.trace, 0 * 512 + t, 0 * 512 + 512);
         if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);
         sm100::tc_fence_after();
         if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
@@ -285,7 +287,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           if (sm100::elect_one()) mma1(nxt.item_c & 1, (t + 1) & 1, 0);
           __syncwarp();
         }
+        if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
         sm100::mbar_wait(&p_full[1], t & 1);
+        if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
           mma2(st, 1, false);
@@ -303,6 +307,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);
         }
         __syncwarp();
+        if (lane == 0) sm100::trace_event(args.trace, 3 * 512 + t, 3 * 512 + 512);
         cur = nxt;
         ++t;
       }
@@ -328,6 +333,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const bool key_valid = kt * kTile + (int)row < nk;
       for (int i = 0; i < nqt; ++i, ++t) {
         sm100::mbar_wait(&s_full[qh], t & 1);
+        if (lane == 0 && quarter == 0) sm100::trace_event(args.trace, (4 + 2 * qh) * 512 + t, (5 + 2 * qh) * 512);
         sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
         uint8_t* dsr = ds_row + (t & 1) * C::kDSBytes;
@@ -357,6 +363,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
+        if (lane == 0 && quarter == 0) sm100::trace_event(args.trace, (5 + 2 * qh) * 512 + t, (6 + 2 * qh) * 512);
       }
     }
   } else if (warp < C::kWarpTMA) {
@@ -374,7 +381,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const size_t zh = (size_t)(b * args.H + h);
       for (int i = 0; i < nqt; ++i, ++t) {
-        sm100::mbar_wait(dq_full, t & 1);
+        sm100::mbar_wait_sleep(dq_full, t & 1);
         sm100::tc_fence_after();
         uint32_t r0[32], r1[32];
         sm100::tmem_ld32(tmem + lane_addr + C::kColDQ, r0);
@@ -398,7 +405,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         }
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
-      sm100::mbar_wait(acc_full, item_c & 1);
+      sm100::mbar_wait_sleep(acc_full, item_c & 1);
       sm100::tc_fence_after();
       const int key = kt * kTile + (int)row;
       const bool key_valid = key < nk;

@@ -139,7 +139,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       if (nkt <= 0) continue;
       const int zh = b * args.H + h;
       const uint32_t qb = c & 1, qph = (c >> 1) & 1;
-      sm100::mbar_wait(&q_empty[qb], qph ^ 1);
+      sm100::mbar_wait_sleep(&q_empty[qb], qph ^ 1);
       if (sm100::elect_one()) {
         sm100::mbar_arrive_expect_tx(&q_full[qb], C::kTileBytes);
         uint8_t* qs = smem + C::kQOff + qb * C::kTileBytes;
@@ -150,7 +150,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       __syncwarp();
       for (int j = 0; j < nkt; ++j, ++kv_it) {
         const uint32_t st = kv_it % C::kStages, ph = (kv_it / C::kStages) & 1;
-        sm100::mbar_wait(&kv_empty[st], ph ^ 1);
+        sm100::mbar_wait_sleep(&kv_empty[st], ph ^ 1);
         if (sm100::elect_one()) {
           sm100::trace_event(args.trace, kv_it, 512);
           uint8_t* ks = smem + C::kKOff + st * C::kTileBytes;

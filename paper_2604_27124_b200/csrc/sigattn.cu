@@ -198,6 +198,7 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   a.dq_acc = dq_acc;
   a.dk = dk;
   a.dv = dv;
+  a.trace = g_trace;
   using C = BwdCfg<D>;
   auto kern = sigattn_bwd_kernel<D, kBf16>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;

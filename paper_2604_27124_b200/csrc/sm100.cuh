@@ -54,9 +54,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
-// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
-// or the hint (ns) expires, instead of spinning on issue slots the compute warps need.
+// mbarrier.try_wait without a suspend hint returns promptly (spin); with a hint the thread sleeps in
+// hardware (NANOSLEEP.SYNCS) and wakes up to ~500 cycles late.  Latency-critical waits spin.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
@@ -67,13 +78,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Wait until the phase with the given parity has completed.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+template <bool kSleep>
+__device__ __forceinline__ void mbar_wait_impl(uint64_t* bar, uint32_t parity) {
+  auto try_once = [&]() { return kSleep ? mbar_try_wait_sleep(bar, parity) : mbar_try_wait(bar, parity); };
 #if SIGATTN_WATCHDOG
-  if (mbar_try_wait(bar, parity)) return;
+  if (try_once()) return;
   const long long t0 = clock64();
   uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
+  while (!try_once()) {
     if ((++n & 1023u) == 0 && clock64() - t0 > (1ll << 35)) {  // ~17 s: a lost phase, not a slow kernel
       printf("sigattn watchdog: block %d thread %d stuck on mbarrier %p parity %u\n", blockIdx.x, threadIdx.x,
              bar, parity);
@@ -81,10 +93,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
   }
 #else
-  while (!mbar_try_wait(bar, parity)) {
+  while (!try_once()) {
   }
 #endif
 }
+// Wait until the phase with the given parity has completed (spinning).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_impl<false>(bar, parity); }
+// Same, sleeping in hardware between polls (for waits that are long and not latency critical).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) { mbar_wait_impl<true>(bar, parity); }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
