@@ -52,14 +52,15 @@ template <int D>
 struct BwdCfg {
   static_assert(D == 64, "fused backward: d = 64 TMEM plan");
   static constexpr int kTileBytes = kTile * D * 2;           // 16 KB
+  static constexpr int kQStages = 3;                         // Q_i + dO_i ring
   static constexpr int kKOff = 0;                            // K[2]
   static constexpr int kVOff = kKOff + 2 * kTileBytes;       // V[2]
-  static constexpr int kQOff = kVOff + 2 * kTileBytes;       // Q[2]
-  static constexpr int kDOOff = kQOff + 2 * kTileBytes;      // dO[2]
-  static constexpr int kDSOff = kDOOff + 2 * kTileBytes;     // dS^T[2]: 2 halves of [128 keys][64 q]
+  static constexpr int kQOff = kVOff + 2 * kTileBytes;       // Q[kQStages]
+  static constexpr int kDOOff = kQOff + kQStages * kTileBytes;      // dO[kQStages]
+  static constexpr int kDSOff = kDOOff + kQStages * kTileBytes;     // dS^T[2]: 2 halves of [128 keys][64 q]
   static constexpr int kDSBytes = 2 * kTile * 128;
   static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
-  static constexpr int kNumBars = 2 + 2 + 2 + 2 + 2 + 2 + 2 + 1 + 1 + 1 + 1;
+  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kThreads = 512;
   static constexpr int kWarpEpi = 8, kWarpTMA = 12, kWarpMMA = 13, kWarpAlloc = 14;
@@ -104,14 +105,14 @@ struct TileIter {
 // One 32-query chunk of a key row: P^T and dS^T = P^T (1 - P^T) dP^T, packed to 16 bits.
 // kMask: columns e >= nvalid (padded queries) or an invalid key row give P = dS = 0.
 template <bool kMask, bool kBf16>
-__device__ __forceinline__ void bwd_row32(const uint32_t (&s)[32], const uint32_t (&dp)[32], uint32_t (&pp)[16],
-                                          uint32_t (&dd)[16], float a2, float b2, int nvalid) {
+__device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
+                                          float a2, float b2, bool key_valid, int nvalid) {
+  sigma_row<16, kMask>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
 #pragma unroll
-  for (int e = 0; e < 32; e += 2) {
-    float p0, p1, u0, u1, d0, d1;
-    sigma2(__uint_as_float(s[e]), __uint_as_float(s[e + 1]), a2, b2, p0, p1);
+  for (int e = 0; e < 16; e += 2) {
+    float p0 = v[e], p1 = v[e + 1], u0, u1, d0, d1;
     ffma2(u0, u1, p0, p1, -p0, -p1, p0, p1);                   // p (1 - p)
-    fmul2(d0, d1, u0, u1, __uint_as_float(dp[e]), __uint_as_float(dp[e + 1]));
+    fmul2(d0, d1, u0, u1, dp[e], dp[e + 1]);
     if constexpr (kMask) {
       p0 = (e < nvalid) ? p0 : 0.0f;
       d0 = (e < nvalid) ? d0 : 0.0f;
@@ -134,15 +135,15 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* kv_full = bars + 0;        // [2]
   uint64_t* kv_empty = bars + 2;       // [2]
-  uint64_t* qdo_full = bars + 4;       // [2]
-  uint64_t* qdo_empty = bars + 6;      // [2]
-  uint64_t* s_full = bars + 8;         // [2] per query half
-  uint64_t* p_full = bars + 10;        // [2] per query half
-  uint64_t* ds_free = bars + 12;       // [2] per dS buffer
-  uint64_t* dq_full = bars + 14;
-  uint64_t* dq_empty = bars + 15;
-  uint64_t* acc_full = bars + 16;
-  uint64_t* acc_empty = bars + 17;
+  uint64_t* qdo_full = bars + 4;                  // [kQStages]
+  uint64_t* qdo_empty = qdo_full + C::kQStages;   // [kQStages]
+  uint64_t* s_full = qdo_empty + C::kQStages;     // [2] per query half
+  uint64_t* p_full = s_full + 2;                  // [2] per query half
+  uint64_t* ds_free = p_full + 2;                 // [2] per dS buffer
+  uint64_t* dq_full = ds_free + 2;
+  uint64_t* dq_empty = dq_full + 1;
+  uint64_t* acc_full = dq_empty + 1;
+  uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -152,11 +153,13 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
-      sm100::mbar_init(&qdo_full[i], 1);
-      sm100::mbar_init(&qdo_empty[i], 1);
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&p_full[i], 4);
       sm100::mbar_init(&ds_free[i], 1);
+    }
+    for (int i = 0; i < C::kQStages; ++i) {
+      sm100::mbar_init(&qdo_full[i], 1);
+      sm100::mbar_init(&qdo_empty[i], 1);
     }
     sm100::mbar_init(dq_full, 1);
     sm100::mbar_init(dq_empty, 4);
@@ -188,7 +191,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       if (nqt <= 0) continue;
       const int zh = b * args.H + h;
       const uint32_t kvb = kv_c & 1;
-      sm100::mbar_wait_sleep(&kv_empty[kvb], ((kv_c >> 1) & 1) ^ 1);
+      sm100::mbar_wait_backoff(&kv_empty[kvb], ((kv_c >> 1) & 1) ^ 1);
       if (sm100::elect_one()) {
         sm100::mbar_arrive_expect_tx(&kv_full[kvb], 2 * C::kTileBytes);
         sm100::tma_load_3d(smem + C::kKOff + kvb * C::kTileBytes, &tmK, &kv_full[kvb], 0, kt * kTile, zh, pol_kv);
@@ -196,8 +199,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       __syncwarp();
       for (int i = 0; i < nqt; ++i, ++t) {
-        const uint32_t st = t & 1;
-        sm100::mbar_wait_sleep(&qdo_empty[st], ((t >> 1) & 1) ^ 1);
+        const uint32_t st = t % C::kQStages;
+        sm100::mbar_wait_backoff(&qdo_empty[st], ((t / C::kQStages) & 1) ^ 1);
         if (sm100::elect_one()) {
           sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kTileBytes);
           sm100::tma_load_3d(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q);
@@ -273,7 +276,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       while (cur.valid) {
         TileIter nxt = cur;
         nxt.advance(args.items);
-        const uint32_t st = t & 1, kvb = cur.item_c & 1;
+        const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1;
+        const uint32_t st1 = (t + 1) % C::kQStages, ph1 = ((t + 1) / C::kQStages) & 1;
         sm100::mbar_wait(&p_full[0], t & 1);
         if (lane == 0) sm100::trace_event(args.trace, 0 * 512 + t, 0 * 512 + 512);
         if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);
@@ -282,9 +286,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         __syncwarp();
         if (nxt.valid) {
           if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
-          sm100::mbar_wait(&qdo_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
+          sm100::mbar_wait(&qdo_full[st1], ph1);
           sm100::tc_fence_after();
-          if (sm100::elect_one()) mma1(nxt.item_c & 1, (t + 1) & 1, 0);
+          if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 0);
           __syncwarp();
         }
         if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
@@ -293,16 +297,16 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
           mma2(st, 1, false);
+          sm100::mma_commit(&qdo_empty[st]);                       // last reader of Q_i, dO_i
           if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
-          if (nxt.valid) mma1(nxt.item_c & 1, (t + 1) & 1, 1);     // half 1 of the next tile before dQ
+          if (nxt.valid) mma1(nxt.item_c & 1, st1, 1);             // half 1 of the next tile before dQ
         }
         __syncwarp();
         sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
-          mma_dq(kvb, st);
-          sm100::mma_commit(&qdo_empty[st]);
-          sm100::mma_commit(&ds_free[st]);
+          mma_dq(kvb, t & 1);
+          sm100::mma_commit(&ds_free[t & 1]);
           sm100::mma_commit(dq_full);
           if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);
         }
@@ -319,7 +323,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
     const uint32_t s_col = C::kColS + qh * 64, dp_col = C::kColDP + qh * 64;
-    uint8_t* ds_row = smem + C::kDSOff + qh * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128;
+    const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + qh * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128);
     uint32_t t = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
@@ -328,34 +332,37 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const float bias = args.bias_per_seq ? args.bias_per_seq[b] : args.bias;
-      const float a2 = -args.scale * kLog2e;
-      const float b2 = -bias * kLog2e;
+      const float a2 = args.scale * kLog2e;    // t = x log2 e
+      const float b2 = bias * kLog2e;
       const bool key_valid = kt * kTile + (int)row < nk;
+      const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       for (int i = 0; i < nqt; ++i, ++t) {
         sm100::mbar_wait(&s_full[qh], t & 1);
         if (lane == 0 && quarter == 0) sm100::trace_event(args.trace, (4 + 2 * qh) * 512 + t, (5 + 2 * qh) * 512);
         sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
-        uint8_t* dsr = ds_row + (t & 1) * C::kDSBytes;
+        const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
         const int q0 = i * kTile + (int)qh * 64;
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          uint32_t s[32], dp[32];
-          sm100::tmem_ld32(tmem + lane_addr + s_col + ch * 32, s);
-          sm100::tmem_ld32(tmem + lane_addr + dp_col + ch * 32, dp);
-          sm100::tmem_wait_ld_dep(s);
-          sm100::tmem_wait_ld_dep(dp);
-          // valid query columns in this chunk (0 for a padded key row)
-          const int nvalid = key_valid ? nq - (q0 + ch * 32) : 0;
-          uint32_t pp[16], dd[16];
-          if (nvalid >= 32) bwd_row32<false, kBf16>(s, dp, pp, dd, a2, b2, nvalid);
-          else bwd_row32<true, kBf16>(s, dp, pp, dd, a2, b2, nvalid);
-          sm100::tmem_st16(tmem + lane_addr + s_col + ch * 16, pp);
-          sm100::tmem_st16(tmem + lane_addr + dp_col + ch * 16, dd);
+        for (int ch = 0; ch < 4; ++ch) {   // 16 query columns per step (register budget)
+          float s[16], dp[16];
+          sm100::tmem_ld16(tmem + lane_addr + s_col + ch * 16, s);
+          sm100::tmem_ld16(tmem + lane_addr + dp_col + ch * 16, dp);
+          sm100::tmem_wait_ld_dep16(s);
+          sm100::tmem_wait_ld_dep16(dp);
+          // valid query columns in this step; the masked variant is chosen warp-uniformly (it also
+          // zeroes the rows of padded keys)
+          const int ncol = nq - (q0 + ch * 16);
+          uint32_t pp[8], dd[8];
+          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16);
+          else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
+          sm100::tmem_st8(tmem + lane_addr + s_col + ch * 8, pp);
+          sm100::tmem_st8(tmem + lane_addr + dp_col + ch * 8, dd);
+          // dS^T row into the swizzled smem tile: 16 queries = 32 B = 16-byte chunks 2ch, 2ch+1
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t chunk = (uint32_t)(ch * 4 + u) ^ (row & 7);
-            *reinterpret_cast<uint4*>(dsr + chunk * 16) = make_uint4(dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t chunk = (uint32_t)(ch * 2 + u) ^ (row & 7);
+            sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
           }
         }
         sm100::tmem_wait_st();
@@ -381,7 +388,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const size_t zh = (size_t)(b * args.H + h);
       for (int i = 0; i < nqt; ++i, ++t) {
-        sm100::mbar_wait_sleep(dq_full, t & 1);
+        sm100::mbar_wait_backoff(dq_full, t & 1);
         sm100::tc_fence_after();
         uint32_t r0[32], r1[32];
         sm100::tmem_ld32(tmem + lane_addr + C::kColDQ, r0);
@@ -405,7 +412,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         }
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
-      sm100::mbar_wait_sleep(acc_full, item_c & 1);
+      sm100::mbar_wait_backoff(acc_full, item_c & 1);
       sm100::tc_fence_after();
       const int key = kt * kTile + (int)row;
       const bool key_valid = key < nk;

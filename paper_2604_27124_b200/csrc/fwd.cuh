@@ -8,7 +8,7 @@
 //               (P aliased onto the first half of its own S columns), then the epilogue for
 //               its quarter of the O columns (padded query rows written as exact 0).
 //   warp 16     TMA producer: Q tile (double-buffered) and a K/V ring of kStages tiles
-//   warp 17     MMA issuer (one elected thread): S = Q K^T (SS, both K-major) -> TMEM S[2]
+//   warp 17     MMA issuer (one elected thread): S = Q K^T (SS, both K-major) -> TMEM S[3] ring
 //                                                O += P V  (TS, P from TMEM, V MN-major) -> TMEM O
 //   warp 18     TMEM allocator
 // Work items (b, h, q-tile) come from a device work list sorted longest-first (LPT), built
@@ -45,7 +45,7 @@ struct FwdCfg {
   static constexpr int kKOff = kQOff + 2 * kTileBytes;      // K[kStages]
   static constexpr int kVOff = kKOff + kStages * kTileBytes;
   static constexpr int kBarOff = kVOff + kStages * kTileBytes;
-  static constexpr int kNumBars = 2 + 2 + 3 * kStages + 2 + 2 + 2;
+  static constexpr int kNumBars = 2 + 2 + 4 * kStages + 3 + 3 + 2;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;  // + alignment slack
   static constexpr int kNumWG = 4;                          // sigmoid warpgroups: warps [0, 4 kNumWG)
   // Single-thread roles sit in the HIGHEST warp ids: the warp scheduler favours high warp ids, so
@@ -54,19 +54,22 @@ struct FwdCfg {
   static constexpr int kThreads = 32 * (4 * kNumWG + 4);
   static constexpr uint32_t kTmemCols = 512;
   // TMEM columns
-  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
+  // S ring of kSBuf 128-column fp32 buffers (P aliased inside each), then O.
+  static constexpr uint32_t kSBuf = 3;
+  static constexpr uint32_t kColO = 128 * kSBuf;
+  static_assert(kColO + D <= kTmemCols, "TMEM budget");
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // 32 scores of one row -> 16 packed 16-bit P values; kMask zeroes columns e >= nvalid (padded keys).
 template <bool kMask, bool kBf16>
-__device__ __forceinline__ void sigmoid_row32(const uint32_t (&r)[32], uint32_t (&pk)[16], float a2, float b2,
+__device__ __forceinline__ void sigmoid_row32(float (&v)[32], uint32_t (&pk)[16], float a, float c, bool row_valid,
                                               int nvalid) {
+  sigma_row<32, kMask>(v, a, c, row_valid, nvalid);
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
-    float p0, p1;
-    sigma2(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), a2, b2, p0, p1);
+    float p0 = v[e], p1 = v[e + 1];
     if constexpr (kMask) {
       p0 = (e < nvalid) ? p0 : 0.0f;
       p1 = (e + 1 < nvalid) ? p1 : 0.0f;
@@ -87,10 +90,11 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* q_empty = bars + 2;         // [2]
   uint64_t* k_full = bars + 4;          // [kStages]
   uint64_t* v_full = k_full + C::kStages;
-  uint64_t* kv_empty = v_full + C::kStages;
-  uint64_t* s_full = kv_empty + C::kStages;  // [2]
-  uint64_t* p_full = s_full + 2;             // [2]
-  uint64_t* o_full = p_full + 2;             // [1]
+  uint64_t* k_empty = v_full + C::kStages;   // K slot free: its S MMA completed
+  uint64_t* v_empty = k_empty + C::kStages;  // V slot free: its PV MMA completed
+  uint64_t* s_full = v_empty + C::kStages;   // [kSBuf]
+  uint64_t* p_full = s_full + C::kSBuf;      // [kSBuf]
+  uint64_t* o_full = p_full + C::kSBuf;      // [1]
   uint64_t* o_empty = o_full + 1;            // [1]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
@@ -101,13 +105,16 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&q_full[i], 1);
       sm100::mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < (int)C::kSBuf; ++i) {
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&p_full[i], 4 * C::kNumWG);   // one arrival per sigmoid warp
     }
     for (int i = 0; i < C::kStages; ++i) {
       sm100::mbar_init(&k_full[i], 1);
       sm100::mbar_init(&v_full[i], 1);
-      sm100::mbar_init(&kv_empty[i], 1);
+      sm100::mbar_init(&k_empty[i], 1);
+      sm100::mbar_init(&v_empty[i], 1);
     }
     sm100::mbar_init(o_full, 1);
     sm100::mbar_init(o_empty, 4 * C::kNumWG);
@@ -139,7 +146,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       if (nkt <= 0) continue;
       const int zh = b * args.H + h;
       const uint32_t qb = c & 1, qph = (c >> 1) & 1;
-      sm100::mbar_wait_sleep(&q_empty[qb], qph ^ 1);
+      sm100::mbar_wait_backoff(&q_empty[qb], qph ^ 1);
       if (sm100::elect_one()) {
         sm100::mbar_arrive_expect_tx(&q_full[qb], C::kTileBytes);
         uint8_t* qs = smem + C::kQOff + qb * C::kTileBytes;
@@ -150,15 +157,21 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       __syncwarp();
       for (int j = 0; j < nkt; ++j, ++kv_it) {
         const uint32_t st = kv_it % C::kStages, ph = (kv_it / C::kStages) & 1;
-        sm100::mbar_wait_sleep(&kv_empty[st], ph ^ 1);
+        // K and V slots are released separately (K after its S MMA, V after its PV MMA), so the
+        // S look-ahead never waits for a PV that is itself waiting for sigma.
+        sm100::mbar_wait_backoff(&k_empty[st], ph ^ 1);
         if (sm100::elect_one()) {
           sm100::trace_event(args.trace, kv_it, 512);
           uint8_t* ks = smem + C::kKOff + st * C::kTileBytes;
-          uint8_t* vs = smem + C::kVOff + st * C::kTileBytes;
           sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
             sm100::tma_load_3d(ks + s * (kTile * 128), &tmK, &k_full[st], s * 64, j * kTile, zh, pol_kv);
+        }
+        __syncwarp();
+        sm100::mbar_wait_backoff(&v_empty[st], ph ^ 1);
+        if (sm100::elect_one()) {
+          uint8_t* vs = smem + C::kVOff + st * C::kTileBytes;
           sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
@@ -187,7 +200,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::mbar_wait(&k_full[st], (kvi / C::kStages) & 1);
         sm100::tc_fence_after();
         const uint32_t ka = k_base + st * C::kTileBytes;
-        const uint32_t d_s = tmem + ((si & 1) ? C::kColS1 : C::kColS0);
+        const uint32_t d_s = tmem + (si % C::kSBuf) * 128;
         if (sm100::elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
@@ -195,23 +208,28 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             sm100::mma_ss(d_s, sm100::make_sdesc_sw128(qa + off, 16, 1024),
                           sm100::make_sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
           }
-          sm100::mma_commit(&s_full[si & 1]);
+          sm100::mma_commit(&s_full[si % C::kSBuf]);
+          sm100::mma_commit(&k_empty[st]);
           sm100::trace_event(args.trace, 512 + si, 1024);
         }
         __syncwarp();
       };
+      // S runs two key tiles ahead of PV and is issued BEFORE the PV of the current tile:
+      // S(j+2) reuses the buffer of P(j-1), read by PV(j-1) issued earlier (tcgen05 ops of one
+      // thread execute in order), so it never waits for sigma(j).
       issue_s(kv_it, s_it);
+      if (nkt > 1) issue_s(kv_it + 1, s_it + 1);
       for (int j = 0; j < nkt; ++j) {
-        if (j + 1 < nkt) issue_s(kv_it + j + 1, s_it + j + 1);
+        if (j + 2 < nkt) issue_s(kv_it + j + 2, s_it + j + 2);
         const uint32_t si = s_it + j;
-        sm100::mbar_wait(&p_full[si & 1], (si >> 1) & 1);
+        sm100::mbar_wait(&p_full[si % C::kSBuf], (si / C::kSBuf) & 1);
         if (j == 0) sm100::mbar_wait(o_empty, (c & 1) ^ 1);   // epilogue drained the previous O
         const uint32_t kvi = kv_it + j;
         const uint32_t st = kvi % C::kStages;
         sm100::mbar_wait(&v_full[st], (kvi / C::kStages) & 1);
         sm100::tc_fence_after();
         const uint32_t va = v_base + st * C::kTileBytes;
-        const uint32_t p_col = (si & 1) ? C::kColS1 : C::kColS0;
+        const uint32_t p_col = (si % C::kSBuf) * 128;
         if (sm100::elect_one()) {
           sm100::trace_event(args.trace, 1024 + si, 1536);
 #pragma unroll
@@ -222,7 +240,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                           sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
                           (j > 0 || kk > 0) ? 1u : 0u);
           }
-          sm100::mma_commit(&kv_empty[st]);
+          sm100::mma_commit(&v_empty[st]);
           sm100::trace_event(args.trace, 1536 + si, 2048);
         }
         __syncwarp();
@@ -250,24 +268,26 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const float bias = args.bias_per_seq ? args.bias_per_seq[b] : args.bias;
-      const float a2 = -args.scale * kLog2e;   // sigma(x) = 1 / (1 + 2^(-x log2 e))
-      const float b2 = -bias * kLog2e;
+      const float a2 = args.scale * kLog2e;    // t = x log2 e = s (alpha log2 e) + b log2 e
+      const float b2 = bias * kLog2e;
+      const bool row_valid = qt * kTile + (int)row < nq;
       for (int j = 0; j < nkt; ++j) {
         const uint32_t si = s_it + j;
-        const uint32_t col = ((si & 1) ? C::kColS1 : C::kColS0) + g * 32;
-        sm100::mbar_wait(&s_full[si & 1], (si >> 1) & 1);
+        const uint32_t col = (si % C::kSBuf) * 128 + g * 32;
+        sm100::mbar_wait(&s_full[si % C::kSBuf], (si / C::kSBuf) & 1);
         if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 2048 + si, 2560);
         sm100::tc_fence_after();
         const int nvalid = nk - (j * kTile + (int)g * 32);   // valid keys in this warpgroup's 32 columns
-        uint32_t r[32], pk[16];
+        float r[32];
+        uint32_t pk[16];
         sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
-        if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, nvalid);
-        else sigmoid_row32<true, kBf16>(r, pk, a2, b2, nvalid);
+        if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+        else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
         sm100::tmem_st16(tmem + lane_addr + col, pk);
         sm100::tmem_wait_st();
         sm100::tc_fence_before();
         __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&p_full[si & 1]);
+        if (lane == 0) sm100::mbar_arrive(&p_full[si % C::kSBuf]);
         if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 2560 + si, 3072);
         if (lane == 0 && warp == 4 * C::kNumWG - 1) sm100::trace_event(args.trace, 3072 + si, 3584);
       }

@@ -101,6 +101,29 @@ __device__ __forceinline__ void mbar_wait_impl(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_impl<false>(bar, parity); }
 // Same, sleeping in hardware between polls (for waits that are long and not latency critical).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) { mbar_wait_impl<true>(bar, parity); }
+// Poll with a short nanosleep back-off: ~100-200 cycles of wake-up latency, few issue slots.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+#if SIGATTN_WATCHDOG
+  const long long t0 = clock64();
+  uint32_t n = 0;
+#endif
+  while (true) {
+    __nanosleep(64);
+    if (mbar_try_wait(bar, parity)) return;
+#if SIGATTN_WATCHDOG
+    if ((++n & 1023u) == 0 && clock64() - t0 > (1ll << 35)) {
+      printf("sigattn watchdog: block %d thread %d stuck on mbarrier %p parity %u\n", blockIdx.x, threadIdx.x,
+             bar, parity);
+      __trap();
+    }
+#endif
+  }
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -240,6 +263,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&r)[32]) {
+  tmem_ld32(taddr, reinterpret_cast<uint32_t(&)[32]>(r));
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -296,6 +322,24 @@ __device__ __forceinline__ void tmem_wait_ld_dep(uint32_t (&r)[32]) {
                  "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
                  "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
                  "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld_dep(float (&r)[32]) {
+  tmem_wait_ld_dep(reinterpret_cast<uint32_t(&)[32]>(r));
+}
+__device__ __forceinline__ void tmem_ld32_sync(uint32_t taddr, float (&r)[32]) {
+  tmem_ld32_sync(taddr, reinterpret_cast<uint32_t(&)[32]>(r));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
+  tmem_ld16(taddr, reinterpret_cast<uint32_t(&)[16]>(r));
+}
+__device__ __forceinline__ void tmem_wait_ld_dep16(float (&r)[16]) {
+  uint32_t(&u)[16] = reinterpret_cast<uint32_t(&)[16]>(r);
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]), "+r"(u[7]),
+                 "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]), "+r"(u[14]),
+                 "+r"(u[15])
                :
                : "memory");
 }

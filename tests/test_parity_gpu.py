@@ -204,3 +204,21 @@ def test_c3_full_size_sampled():
             g = f64(got[bb, hh])[rows]
             err = relerr(g, ref)
             assert err <= BF16_TOL, f"{name} (b={bb}, h={hh}) rel err {err}"
+
+
+@pytest.mark.parametrize("bias,scale", [(0.0, None), (3.0, None), (-1.0, 0.5), (-30.0, None)])
+def test_sigmoid_slow_and_saturated_paths(bias, scale):
+    """Logits above -2 (bias 0 / +3 / large scale) exercise the exact-range sigma path; bias -30
+    saturates to P ~ 0.  Both kernels must stay within the bf16 bound."""
+    sa = _sa()
+    cfg = I.Config("slowpath", B=2, H=2, N=256, d=64, lengths=[256, 150], seed=21)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    alpha = 1.0 / math.sqrt(cfg.d) if scale is None else scale
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, bias)
+    dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, bias)
+    bias_np = np.full(cfg.B, bias)
+    ro = oracle.fwd(f64(q), f64(k), f64(v), cfg.nq, cfg.nk, alpha, bias_np)
+    rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, alpha, bias_np)
+    for name, got, ref in (("o", o, ro), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+        err = relerr(f64(got), ref)
+        assert err <= BF16_TOL, f"{name} rel err {err} (bias={bias}, scale={scale})"
