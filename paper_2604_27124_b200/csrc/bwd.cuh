@@ -2,31 +2,33 @@
 //
 // The paper splits the backward into a dQ kernel (Alg. 2) and a dK/dV kernel
 // (Alg. 3), each recomputing sigma.  Here the two are fused into ONE key-tile-owned
-// pass: every (b, h, key tile) item keeps K_j, V_j resident and loops over
-// the valid 128-query tiles i, each processed as two 64-query halves q in {0, 1}:
-//     S^T_q  = K_j Q_iq^T,   dP^T_q = V_j dO_iq^T                (Alg. 3)
-//     P^T_q  = mask . sigma(alpha S^T_q + b)
-//     dS^T_q = P^T_q (1 - P^T_q) dP^T_q
-//     dV_j  += P^T_q dO_iq,   dK_j += dS^T_q Q_iq  on chip, atomic-free
-//     dQ_i  += dS_i K_j  (both halves, M = 128)  fp32 partial per key tile
+// pass: every (b, h, key tile j) item keeps K_j, V_j resident and loops
+// over the valid 128-query tiles i:
+//     S^T  = K_j Q_i^T,   dP^T = V_j dO_i^T               (Alg. 3)     SS, N = 128
+//     P^T  = mask . sigma(alpha S^T + b)
+//     dS^T = P^T (1 - P^T) dP^T
+//     dV_j += P^T dO_i      (A = P^T from TMEM)                    TS, N = d
+//     dK_j += dS^T Q_i      (A = dS^T from smem)                    SS, N = d
+//     dQ_i  = dS K_j        (A = dS from smem, MN-major)  fp32 partial,    SS, N = d
+//                                                                    reduce-added into a workspace
 // alpha is applied once in the epilogues.  sigma is evaluated once per element and
 // the tensor work is the credited 10 d per (query, key) pair.
 //
-// CTA roles (512 threads, persistent, one CTA per SM; single-thread roles in the highest warp ids,
+// Overlap: P^T and dS^T do not live in the S^T / dP^T columns, so as soon as the compute warps
+// have consumed S^T_i / dP^T_i the MMA warp issues S^T_{i+1}, dP^T_{i+1} and only then the dV / dK
+// / dQ MMAs of tile i -- the compute warps work on tile i+1 while the tensor core finishes tile i.
+//
+// CTA roles (768 threads, persistent, one CTA per SM; single-thread roles in the highest warp ids,
 // which the warp scheduler favours):
-//   warps 0-3   compute warpgroup for query half 0; warps 4-7 for half 1 (thread = key row)
-//   warps 8-11  epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
+//   warps 0-15  four compute warpgroups; thread = key row (TMEM lane), WG g = queries [32g, 32g+32)
+//   warps 16-19 epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
 //               dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
-//   warp 12     TMA: K_j, V_j (2 slots), Q_i + dO_i (2 stages)
-//   warp 13     MMA issuer (one elected thread); issue order per tile i (look-ahead one tile):
-//                 dV/dK(i, q0) | S,dP(i+1, q0) | dV/dK(i, q1) | S,dP(i+1, q1) | dQ(i)
-//               so warpgroup q0 computes tile i+1 while warpgroup q1 still computes tile i.
-//   warp 14     TMEM allocator
-// TMEM (d = 64): S^T_q0 [0,64) S^T_q1 [64,128) dP^T_q0 [128,192) dP^T_q1 [192,256)
-//                dV [256,320) dK [320,384) dQ [384,448).
-// P^T / dS^T (16-bit) are written back over the first half of their own S^T / dP^T columns and
-// feed the dV / dK MMAs from TMEM; dS^T also goes to shared memory (128B-swizzled, keys as rows,
-// double-buffered) where the same bytes are the MN-major A operand of dQ = dS K.
+//   warp 20     TMA: K_j, V_j (2 slots), Q_i + dO_i (3 stages)
+//   warp 21     MMA issuer (one elected thread)
+//   warp 22     TMEM allocator
+// TMEM (d = 64): S^T [0,128) dP^T [128,256) P^T (16-bit) [256,320) dV [320,384) dK [384,448) dQ [448,512)
+// Shared memory: dS^T (16-bit, 128B-swizzled, keys as rows, double-buffered) is the K-major A operand
+// of dK and -- the same bytes read MN-major -- the A operand of dQ.
 #pragma once
 #include "fwd.cuh"
 #include "sigmoid.cuh"
@@ -60,12 +62,14 @@ struct BwdCfg {
   static constexpr int kDSOff = kDOOff + kQStages * kTileBytes;     // dS^T[2]: 2 halves of [128 keys][64 q]
   static constexpr int kDSBytes = 2 * kTile * 128;
   static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
-  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1;
+  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 1 + 1 + 1 + 2 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
-  static constexpr int kThreads = 512;
-  static constexpr int kWarpEpi = 8, kWarpTMA = 12, kWarpMMA = 13, kWarpAlloc = 14;
+  static constexpr int kNumWG = 4;                           // compute warpgroups
+  static constexpr int kWarpEpi = 4 * kNumWG, kWarpTMA = kWarpEpi + 4, kWarpMMA = kWarpTMA + 1,
+                       kWarpAlloc = kWarpTMA + 2;
+  static constexpr int kThreads = 32 * (kWarpEpi + 8);
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D, kColDQ = 256 + 2 * D;
+  static constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDV = 320, kColDK = 384, kColDQ = 448;
 };
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -101,9 +105,8 @@ struct TileIter {
   }
 };
 
-
-// One 32-query chunk of a key row: P^T and dS^T = P^T (1 - P^T) dP^T, packed to 16 bits.
-// kMask: columns e >= nvalid (padded queries) or an invalid key row give P = dS = 0.
+// 16 query columns of one key row: P^T and dS^T = P^T (1 - P^T) dP^T, packed to 16 bits.
+// kMask: columns e >= nvalid (padded queries) give P = dS = 0 (nvalid = 0 for a padded key row).
 template <bool kMask, bool kBf16>
 __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
                                           float a2, float b2, bool key_valid, int nvalid) {
@@ -125,7 +128,7 @@ __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16],
 }
 
 template <int D, bool kBf16>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
 sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                    const BwdArgs args) {
@@ -133,13 +136,14 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
-  uint64_t* kv_full = bars + 0;        // [2]
-  uint64_t* kv_empty = bars + 2;       // [2]
+  uint64_t* kv_full = bars + 0;                   // [2]
+  uint64_t* kv_empty = bars + 2;                  // [2]
   uint64_t* qdo_full = bars + 4;                  // [kQStages]
   uint64_t* qdo_empty = qdo_full + C::kQStages;   // [kQStages]
-  uint64_t* s_full = qdo_empty + C::kQStages;     // [2] per query half
-  uint64_t* p_full = s_full + 2;                  // [2] per query half
-  uint64_t* ds_free = p_full + 2;                 // [2] per dS buffer
+  uint64_t* s_full = qdo_empty + C::kQStages;     // S^T, dP^T of the current tile in TMEM
+  uint64_t* p_full = s_full + 1;                  // compute warps done: P^T in TMEM, dS^T in smem
+  uint64_t* p_free = p_full + 1;                  // dV MMA finished reading P^T
+  uint64_t* ds_free = p_free + 1;                 // [2] dK / dQ MMAs finished reading dS^T buffer
   uint64_t* dq_full = ds_free + 2;
   uint64_t* dq_empty = dq_full + 1;
   uint64_t* acc_full = dq_empty + 1;
@@ -148,19 +152,21 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 
   const uint32_t warp = sm100::warp_id();
   const uint32_t lane = sm100::lane_id();
+  constexpr uint32_t kComputeWarps = 4 * C::kNumWG;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
-      sm100::mbar_init(&s_full[i], 1);
-      sm100::mbar_init(&p_full[i], 4);
       sm100::mbar_init(&ds_free[i], 1);
     }
     for (int i = 0; i < C::kQStages; ++i) {
       sm100::mbar_init(&qdo_full[i], 1);
       sm100::mbar_init(&qdo_empty[i], 1);
     }
+    sm100::mbar_init(s_full, 1);
+    sm100::mbar_init(p_full, kComputeWarps);
+    sm100::mbar_init(p_free, 1);
     sm100::mbar_init(dq_full, 1);
     sm100::mbar_init(dq_empty, 4);
     sm100::mbar_init(acc_full, 1);
@@ -212,118 +218,110 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
   } else if (warp == C::kWarpMMA) {
     // ===================== MMA issuer (whole warp waits, one elected lane issues) =====================
-    {
-      constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 64, false, false);    // S^T_q, dP^T_q
-      constexpr uint32_t idesc_acc = sm100::make_idesc_f16(kBf16, 128, D, false, true);    // dV, dK (A tmem)
-      constexpr uint32_t idesc_dq = sm100::make_idesc_f16(kBf16, 128, D, true, true);      // dQ (A = dS MN-major)
-      const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
-      const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
-      const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
-      const uint32_t do_base = sm100::smem_u32(smem + C::kDOOff);
-      const uint32_t ds_base = sm100::smem_u32(smem + C::kDSOff);
+    constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 128, false, false);   // S^T, dP^T
+    constexpr uint32_t idesc_dv = sm100::make_idesc_f16(kBf16, 128, D, false, true);     // A tmem, B MN-major
+    constexpr uint32_t idesc_dk = sm100::make_idesc_f16(kBf16, 128, D, false, true);     // A K-major smem
+    constexpr uint32_t idesc_dq = sm100::make_idesc_f16(kBf16, 128, D, true, true);      // A MN-major smem
+    const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
+    const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
+    const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
+    const uint32_t do_base = sm100::smem_u32(smem + C::kDOOff);
+    const uint32_t ds_base = sm100::smem_u32(smem + C::kDSOff);
 
-      // S^T_q = K Q_q^T and dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; both K-major)
-      auto mma1 = [&](uint32_t kvb, uint32_t st, uint32_t q) {
-        const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
-        const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+    // S^T = K Q^T and dP^T = V dO^T  (M = 128 keys, N = 128 queries, K = d; all K-major)
+    auto mma_s = [&](uint32_t kvb, uint32_t st) {
+      const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
+      const uint32_t qa = q_base + st * C::kTileBytes, da = do_base + st * C::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          sm100::mma_ss(tmem + C::kColS + q * 64, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024),
-                        sm100::make_sdesc_sw128(qa + kk * 32, 16, 1024), idesc_s, kk > 0);
+      for (int kk = 0; kk < D / 16; ++kk)
+        sm100::mma_ss(tmem + C::kColS, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024),
+                      sm100::make_sdesc_sw128(qa + kk * 32, 16, 1024), idesc_s, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          sm100::mma_ss(tmem + C::kColDP + q * 64, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024),
-                        sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_s, kk > 0);
-        sm100::mma_commit(&s_full[q]);
-      };
-      // dV += P^T_q dO_q ; dK += dS^T_q Q_q   (M = keys, N = d, K = 64 queries; A from TMEM, B MN-major)
-      auto mma2 = [&](uint32_t st, uint32_t q, bool first) {
-        const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+      for (int kk = 0; kk < D / 16; ++kk)
+        sm100::mma_ss(tmem + C::kColDP, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024),
+                      sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_s, kk > 0);
+      sm100::mma_commit(s_full);
+    };
+
+    TileIter cur;
+    cur.init(args.items, n_items);
+    if (cur.valid) {
+      sm100::mbar_wait(&kv_full[cur.item_c & 1], (cur.item_c >> 1) & 1);
+      sm100::mbar_wait(&qdo_full[0], 0);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) mma_s(cur.item_c & 1, 0);
+      __syncwarp();
+    }
+    uint32_t t = 0;
+    while (cur.valid) {
+      TileIter nxt = cur;
+      nxt.advance(args.items);
+      const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1, buf = t & 1;
+      sm100::mbar_wait(p_full, t & 1);                 // S^T/dP^T(t) consumed; P^T(t), dS^T(t) written
+      if (lane == 0) sm100::trace_event(args.trace, 0 * 512 + t, 0 * 512 + 512);
+      if (nxt.valid) {                                 // next tile's scores first: the compute warps
+        const uint32_t st1 = (t + 1) % C::kQStages;   // start on them while dV/dK/dQ(t) run
+        if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
+        sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) mma_s(nxt.item_c & 1, st1);
+        __syncwarp();
+      }
+      if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
+      if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);   // epilogue read previous dV/dK
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const bool first = cur.i == 0;
+        const uint32_t qa = q_base + st * C::kTileBytes, da = do_base + st * C::kTileBytes;
+        const uint32_t dsa = ds_base + buf * C::kDSBytes;
+        // dV += P^T dO   (M = keys, N = d, K = 128 queries)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + q * 64 + kk * 8,
-                        sm100::make_sdesc_sw128(da + kk * 2048, kTile * 128, 1024), idesc_acc,
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          sm100::mma_ts(tmem + C::kColDV, tmem + C::kColP + kk * 8,
+                        sm100::make_sdesc_sw128(da + kk * 2048, kTile * 128, 1024), idesc_dv,
                         (first && kk == 0) ? 0u : 1u);
+        sm100::mma_commit(p_free);
+        // dK += dS^T Q   (A = dS^T K-major: queries [64h, 64h+64) of each key row live in half h)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + q * 64 + kk * 8,
-                        sm100::make_sdesc_sw128(qa + kk * 2048, kTile * 128, 1024), idesc_acc,
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          sm100::mma_ss(tmem + C::kColDK,
+                        sm100::make_sdesc_sw128(dsa + (kk >> 2) * (kTile * 128) + (kk & 3) * 32, 16, 1024),
+                        sm100::make_sdesc_sw128(qa + kk * 2048, kTile * 128, 1024), idesc_dk,
                         (first && kk == 0) ? 0u : 1u);
-      };
-      // dQ_i = dS K_j   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major smem, B = K MN-major smem)
-      auto mma_dq = [&](uint32_t kvb, uint32_t buf) {
+        sm100::mma_commit(&qdo_empty[st]);             // last readers of Q_i, dO_i
+        if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);
+      }
+      __syncwarp();
+      if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
+      sm100::mbar_wait(dq_empty, (t & 1) ^ 1);         // epilogue drained dQ(t-1)
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
         const uint32_t ka = k_base + kvb * C::kTileBytes;
         const uint32_t dsa = ds_base + buf * C::kDSBytes;
+        // dQ = dS K   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major, B = K MN-major)
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk)
           sm100::mma_ss(tmem + C::kColDQ, sm100::make_sdesc_sw128(dsa + kk * 2048, kTile * 128, 1024),
                         sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024), idesc_dq, kk > 0);
-      };
-
-      TileIter cur;
-      cur.init(args.items, n_items);
-      if (cur.valid) {
-        sm100::mbar_wait(&kv_full[cur.item_c & 1], (cur.item_c >> 1) & 1);
-        sm100::mbar_wait(&qdo_full[0], 0);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) {
-          mma1(cur.item_c & 1, 0, 0);
-          mma1(cur.item_c & 1, 0, 1);
-        }
-        __syncwarp();
+        sm100::mma_commit(&ds_free[buf]);
+        sm100::mma_commit(dq_full);
+        if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);
       }
-      uint32_t t = 0;
-      while (cur.valid) {
-        TileIter nxt = cur;
-        nxt.advance(args.items);
-        const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1;
-        const uint32_t st1 = (t + 1) % C::kQStages, ph1 = ((t + 1) / C::kQStages) & 1;
-        sm100::mbar_wait(&p_full[0], t & 1);
-        if (lane == 0) sm100::trace_event(args.trace, 0 * 512 + t, 0 * 512 + 512);
-        if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
-        __syncwarp();
-        if (nxt.valid) {
-          if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
-          sm100::mbar_wait(&qdo_full[st1], ph1);
-          sm100::tc_fence_after();
-          if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 0);
-          __syncwarp();
-        }
-        if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
-        sm100::mbar_wait(&p_full[1], t & 1);
-        if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) {
-          mma2(st, 1, false);
-          sm100::mma_commit(&qdo_empty[st]);                       // last reader of Q_i, dO_i
-          if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
-          if (nxt.valid) mma1(nxt.item_c & 1, st1, 1);             // half 1 of the next tile before dQ
-        }
-        __syncwarp();
-        sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) {
-          mma_dq(kvb, t & 1);
-          sm100::mma_commit(&ds_free[t & 1]);
-          sm100::mma_commit(dq_full);
-          if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);
-        }
-        __syncwarp();
-        if (lane == 0) sm100::trace_event(args.trace, 3 * 512 + t, 3 * 512 + 512);
-        cur = nxt;
-        ++t;
-      }
+      __syncwarp();
+      if (lane == 0) sm100::trace_event(args.trace, 3 * 512 + t, 3 * 512 + 512);
+      cur = nxt;
+      ++t;
     }
-  } else if (warp < C::kWarpEpi) {
-    // ===================== compute warpgroups (query half qh) =====================
-    const uint32_t qh = warp >> 2;
+  } else if (warp < kComputeWarps) {
+    // ===================== compute warpgroups (queries [32g, 32g + 32)) =====================
+    const uint32_t g = warp >> 2;
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
-    const uint32_t s_col = C::kColS + qh * 64, dp_col = C::kColDP + qh * 64;
-    const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + qh * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128);
+    const uint32_t s_col = C::kColS + g * 32, dp_col = C::kColDP + g * 32, p_col = C::kColP + g * 16;
+    // dS^T smem: query half (g >> 1), 16-byte chunks (g & 1) * 4 + [0, 4) of the 128-byte row
+    const uint32_t ds_row =
+        sm100::smem_u32(smem + C::kDSOff + (g >> 1) * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128);
     uint32_t t = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
@@ -337,14 +335,13 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       for (int i = 0; i < nqt; ++i, ++t) {
-        sm100::mbar_wait(&s_full[qh], t & 1);
-        if (lane == 0 && quarter == 0) sm100::trace_event(args.trace, (4 + 2 * qh) * 512 + t, (5 + 2 * qh) * 512);
-        sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
+        sm100::mbar_wait(s_full, t & 1);
+        if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 4 * 512 + t, 5 * 512);
         sm100::tc_fence_after();
         const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
-        const int q0 = i * kTile + (int)qh * 64;
+        const int q0 = i * kTile + (int)g * 32;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {   // 16 query columns per step (register budget)
+        for (int ch = 0; ch < 2; ++ch) {   // 16 query columns per step (register budget)
           float s[16], dp[16];
           sm100::tmem_ld16(tmem + lane_addr + s_col + ch * 16, s);
           sm100::tmem_ld16(tmem + lane_addr + dp_col + ch * 16, dp);
@@ -356,12 +353,15 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           uint32_t pp[8], dd[8];
           if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16);
           else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
-          sm100::tmem_st8(tmem + lane_addr + s_col + ch * 8, pp);
-          sm100::tmem_st8(tmem + lane_addr + dp_col + ch * 8, dd);
-          // dS^T row into the swizzled smem tile: 16 queries = 32 B = 16-byte chunks 2ch, 2ch+1
+          if (ch == 0) {
+            sm100::mbar_wait(p_free, (t & 1) ^ 1);                   // dV(t-1) finished reading P^T
+            sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dK/dQ(t-2) done with this buffer
+            sm100::tc_fence_after();
+          }
+          sm100::tmem_st8(tmem + lane_addr + p_col + ch * 8, pp);
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const uint32_t chunk = (uint32_t)(ch * 2 + u) ^ (row & 7);
+            const uint32_t chunk = (uint32_t)((g & 1) * 4 + ch * 2 + u) ^ (row & 7);
             sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
           }
         }
@@ -369,8 +369,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
-        if (lane == 0 && quarter == 0) sm100::trace_event(args.trace, (5 + 2 * qh) * 512 + t, (6 + 2 * qh) * 512);
+        if (lane == 0) sm100::mbar_arrive(p_full);
+        if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 5 * 512 + t, 6 * 512);
       }
     }
   } else if (warp < C::kWarpTMA) {
@@ -389,26 +389,30 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const size_t zh = (size_t)(b * args.H + h);
       for (int i = 0; i < nqt; ++i, ++t) {
         sm100::mbar_wait_backoff(dq_full, t & 1);
+        if (lane == 0 && quarter == 0) sm100::trace_event(args.trace, 6 * 512 + t, 7 * 512);
         sm100::tc_fence_after();
-        uint32_t r0[32], r1[32];
-        sm100::tmem_ld32(tmem + lane_addr + C::kColDQ, r0);
-        sm100::tmem_ld32(tmem + lane_addr + C::kColDQ + 32, r1);
-        sm100::tmem_wait_ld_dep(r0);
-        sm100::tmem_wait_ld_dep(r1);
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(dq_empty);
         const int q = i * kTile + (int)row;
-        if (q < nq) {
-          float* dst = args.dq_acc + (zh * args.Nq + q) * D;
+        float* dst = args.dq_acc + (zh * args.Nq + q) * D;
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            red_add_v4(dst + e, alpha * __uint_as_float(r0[e]), alpha * __uint_as_float(r0[e + 1]),
-                       alpha * __uint_as_float(r0[e + 2]), alpha * __uint_as_float(r0[e + 3]));
+        for (int hh = 0; hh < 2; ++hh) {     // two 32-column halves (register budget)
+          float r[2][16];
+          sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + hh * 32, r[0]);
+          sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + hh * 32 + 16, r[1]);
+          sm100::tmem_wait_ld_dep16(r[0]);
+          sm100::tmem_wait_ld_dep16(r[1]);
+          if (hh == 1) {
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(dq_empty);
+          }
+          if (q < nq) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            red_add_v4(dst + 32 + e, alpha * __uint_as_float(r1[e]), alpha * __uint_as_float(r1[e + 1]),
-                       alpha * __uint_as_float(r1[e + 2]), alpha * __uint_as_float(r1[e + 3]));
+            for (int c4 = 0; c4 < 2; ++c4)
+#pragma unroll
+              for (int e = 0; e < 16; e += 4)
+                red_add_v4(dst + hh * 32 + c4 * 16 + e, alpha * r[c4][e], alpha * r[c4][e + 1], alpha * r[c4][e + 2],
+                           alpha * r[c4][e + 3]);
+          }
         }
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
@@ -419,37 +423,33 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const size_t off = (zh * args.Nk + key) * D;
 #pragma unroll
       for (int which = 0; which < 2; ++which) {
-        uint32_t r0[32], r1[32];
         const uint32_t col = which == 0 ? C::kColDV : C::kColDK;
         const float sc = which == 0 ? 1.0f : alpha;
-        sm100::tmem_ld32(tmem + lane_addr + col, r0);
-        sm100::tmem_ld32(tmem + lane_addr + col + 32, r1);
-        sm100::tmem_wait_ld_dep(r0);
-        sm100::tmem_wait_ld_dep(r1);
-        if (which == 1) {
-          sm100::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(acc_empty);
-        }
-        if (key < args.Nk) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(which == 0 ? args.dv : args.dk) + off);
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(which == 0 ? args.dv : args.dk) + off);
 #pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 w;
-            w.x = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r0[e]), sc * __uint_as_float(r0[e + 1])) : 0u;
-            w.y = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r0[e + 2]), sc * __uint_as_float(r0[e + 3])) : 0u;
-            w.z = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r0[e + 4]), sc * __uint_as_float(r0[e + 5])) : 0u;
-            w.w = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r0[e + 6]), sc * __uint_as_float(r0[e + 7])) : 0u;
-            dst[e >> 3] = w;
+        for (int hh = 0; hh < 2; ++hh) {
+          float r[2][16];
+          sm100::tmem_ld16(tmem + lane_addr + col + hh * 32, r[0]);
+          sm100::tmem_ld16(tmem + lane_addr + col + hh * 32 + 16, r[1]);
+          sm100::tmem_wait_ld_dep16(r[0]);
+          sm100::tmem_wait_ld_dep16(r[1]);
+          if (which == 1 && hh == 1) {
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(acc_empty);
           }
+          if (key < args.Nk) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 w;
-            w.x = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r1[e]), sc * __uint_as_float(r1[e + 1])) : 0u;
-            w.y = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r1[e + 2]), sc * __uint_as_float(r1[e + 3])) : 0u;
-            w.z = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r1[e + 4]), sc * __uint_as_float(r1[e + 5])) : 0u;
-            w.w = key_valid ? sm100::pack2<kBf16>(sc * __uint_as_float(r1[e + 6]), sc * __uint_as_float(r1[e + 7])) : 0u;
-            dst[4 + (e >> 3)] = w;
+            for (int c4 = 0; c4 < 2; ++c4)
+#pragma unroll
+              for (int e = 0; e < 16; e += 8) {
+                uint4 w;
+                w.x = key_valid ? sm100::pack2<kBf16>(sc * r[c4][e], sc * r[c4][e + 1]) : 0u;
+                w.y = key_valid ? sm100::pack2<kBf16>(sc * r[c4][e + 2], sc * r[c4][e + 3]) : 0u;
+                w.z = key_valid ? sm100::pack2<kBf16>(sc * r[c4][e + 4], sc * r[c4][e + 5]) : 0u;
+                w.w = key_valid ? sm100::pack2<kBf16>(sc * r[c4][e + 6], sc * r[c4][e + 7]) : 0u;
+                dst[hh * 4 + c4 * 2 + (e >> 3)] = w;
+              }
           }
         }
       }
