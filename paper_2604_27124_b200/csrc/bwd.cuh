@@ -2,33 +2,35 @@
 //
 // The paper splits the backward into a dQ kernel (Alg. 2) and a dK/dV kernel
 // (Alg. 3), each recomputing sigma.  Here the two are fused into ONE key-tile-owned
-// pass: every (b, h, key tile j) item keeps K_j, V_j resident and loops
-// over the valid 128-query tiles i:
-//     S^T  = K_j Q_i^T,   dP^T = V_j dO_i^T               (Alg. 3)     SS, N = 128
-//     P^T  = mask . sigma(alpha S^T + b)
-//     dS^T = P^T (1 - P^T) dP^T
-//     dV_j += P^T dO_i      (A = P^T from TMEM)                    TS, N = d
-//     dK_j += dS^T Q_i      (A = dS^T from smem)                    SS, N = d
-//     dQ_i  = dS K_j        (A = dS from smem, MN-major)  fp32 partial,    SS, N = d
-//                                                                    reduce-added into a workspace
-// alpha is applied once in the epilogues.  sigma is evaluated once per element and
-// the tensor work is the credited 10 d per (query, key) pair.
+// pass: every (b, h, key tile j) item keeps K_j, V_j resident (in shared
+// memory and, copied once by tcgen05.cp, in TMEM) and loops over the valid 128-query tiles i, each
+// processed as two 64-query halves q:
+//     S^T_q  = K_j Q_iq^T,  dP^T_q = V_j dO_iq^T     (Alg. 3)   TS: A = K_j / V_j in TMEM
+//     P^T_q  = mask . sigma(alpha S^T_q + b)
+//     dS^T_q = P^T_q (1 - P^T_q) dP^T_q
+//     dV_j  += P^T_q dO_iq,  dK_j += dS^T_q Q_iq          TS: A = P^T / dS^T in TMEM
+//     dQ_i   = dS_i K_j (both halves)                 SS: A = dS^T smem (MN-major)
+// dQ_i is an fp32 partial per key tile, reduce-added into a workspace; alpha is
+// applied once in the epilogues.  sigma is evaluated once per element; the tensor work is the
+// credited 10 d per (query, key) pair.
 //
-// Overlap: P^T and dS^T do not live in the S^T / dP^T columns, so as soon as the compute warps
-// have consumed S^T_i / dP^T_i the MMA warp issues S^T_{i+1}, dP^T_{i+1} and only then the dV / dK
-// / dQ MMAs of tile i -- the compute warps work on tile i+1 while the tensor core finishes tile i.
+// Pipelining: the MMA warp issues, per tile i,   dV/dK(i, q0) | S,dP(i+1, q0) | dV/dK(i, q1) |
+// S,dP(i+1, q1) | dQ(i)   so the half-0 warps compute tile i+1 while the half-1 warps still
+// compute tile i, and the tensor core always has the other half's work queued.
 //
 // CTA roles (768 threads, persistent, one CTA per SM; single-thread roles in the highest warp ids,
 // which the warp scheduler favours):
-//   warps 0-15  four compute warpgroups; thread = key row (TMEM lane), WG g = queries [32g, 32g+32)
+//   warps 0-15  four compute warpgroups; thread = key row (TMEM lane); WG w = queries [32w, 32w+32),
+//               i.e. WGs 0,1 form query half 0 and WGs 2,3 half 1
 //   warps 16-19 epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
 //               dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
 //   warp 20     TMA: K_j, V_j (2 slots), Q_i + dO_i (3 stages)
-//   warp 21     MMA issuer (one elected thread)
+//   warp 21     MMA issuer (one elected thread); also tcgen05.cp of K_j, V_j into TMEM
 //   warp 22     TMEM allocator
-// TMEM (d = 64): S^T [0,128) dP^T [128,256) P^T (16-bit) [256,320) dV [320,384) dK [384,448) dQ [448,512)
-// Shared memory: dS^T (16-bit, 128B-swizzled, keys as rows, double-buffered) is the K-major A operand
-// of dK and -- the same bytes read MN-major -- the A operand of dQ.
+// TMEM (d = 64): S^T [0,128) dP^T [128,256) dV [256,320) dK [320,384) dQ [384,448) K [448,480) V [480,512)
+// P^T / dS^T (16-bit) overwrite the first half of each warpgroup's own S^T / dP^T columns.
+// Shared memory: dS^T (16-bit, 128B-swizzled, keys as rows, double-buffered) is read MN-major as
+// the A operand of dQ = dS K.
 #pragma once
 #include "fwd.cuh"
 #include "sigmoid.cuh"
@@ -62,14 +64,15 @@ struct BwdCfg {
   static constexpr int kDSOff = kDOOff + kQStages * kTileBytes;     // dS^T[2]: 2 halves of [128 keys][64 q]
   static constexpr int kDSBytes = 2 * kTile * 128;
   static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
-  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 1 + 1 + 1 + 2 + 1 + 1 + 1 + 1;
+  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kNumWG = 4;                           // compute warpgroups
   static constexpr int kWarpEpi = 4 * kNumWG, kWarpTMA = kWarpEpi + 4, kWarpMMA = kWarpTMA + 1,
                        kWarpAlloc = kWarpTMA + 2;
   static constexpr int kThreads = 32 * (kWarpEpi + 8);
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDV = 320, kColDK = 384, kColDQ = 448;
+  static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 320, kColDQ = 384, kColK = 448,
+                            kColV = 480;
 };
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -140,10 +143,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* kv_empty = bars + 2;                  // [2]
   uint64_t* qdo_full = bars + 4;                  // [kQStages]
   uint64_t* qdo_empty = qdo_full + C::kQStages;   // [kQStages]
-  uint64_t* s_full = qdo_empty + C::kQStages;     // S^T, dP^T of the current tile in TMEM
-  uint64_t* p_full = s_full + 1;                  // compute warps done: P^T in TMEM, dS^T in smem
-  uint64_t* p_free = p_full + 1;                  // dV MMA finished reading P^T
-  uint64_t* ds_free = p_free + 1;                 // [2] dK / dQ MMAs finished reading dS^T buffer
+  uint64_t* s_full = qdo_empty + C::kQStages;     // [2] per query half: S^T, dP^T in TMEM
+  uint64_t* p_full = s_full + 2;                  // [2] per query half: P^T, dS^T in TMEM, dS^T in smem
+  uint64_t* ds_free = p_full + 2;                 // [2] dQ MMA finished reading dS^T buffer
   uint64_t* dq_full = ds_free + 2;
   uint64_t* dq_empty = dq_full + 1;
   uint64_t* acc_full = dq_empty + 1;
@@ -159,14 +161,13 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
       sm100::mbar_init(&ds_free[i], 1);
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&p_full[i], kComputeWarps / 2);   // the 8 warps of one query half
     }
     for (int i = 0; i < C::kQStages; ++i) {
       sm100::mbar_init(&qdo_full[i], 1);
       sm100::mbar_init(&qdo_empty[i], 1);
     }
-    sm100::mbar_init(s_full, 1);
-    sm100::mbar_init(p_full, kComputeWarps);
-    sm100::mbar_init(p_free, 1);
     sm100::mbar_init(dq_full, 1);
     sm100::mbar_init(dq_empty, 4);
     sm100::mbar_init(acc_full, 1);
@@ -218,29 +219,55 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
   } else if (warp == C::kWarpMMA) {
     // ===================== MMA issuer (whole warp waits, one elected lane issues) =====================
-    constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 128, false, false);   // S^T, dP^T
-    constexpr uint32_t idesc_dv = sm100::make_idesc_f16(kBf16, 128, D, false, true);     // A tmem, B MN-major
-    constexpr uint32_t idesc_dk = sm100::make_idesc_f16(kBf16, 128, D, false, true);     // A K-major smem
-    constexpr uint32_t idesc_dq = sm100::make_idesc_f16(kBf16, 128, D, true, true);      // A MN-major smem
+    constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 64, false, false);    // S^T_q, dP^T_q
+    constexpr uint32_t idesc_acc = sm100::make_idesc_f16(kBf16, 128, D, false, true);    // dV, dK
+    constexpr uint32_t idesc_dq = sm100::make_idesc_f16(kBf16, 128, D, true, true);      // dQ
     const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
     const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
     const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
     const uint32_t do_base = sm100::smem_u32(smem + C::kDOOff);
     const uint32_t ds_base = sm100::smem_u32(smem + C::kDSOff);
 
-    // S^T = K Q^T and dP^T = V dO^T  (M = 128 keys, N = 128 queries, K = d; all K-major)
-    auto mma_s = [&](uint32_t kvb, uint32_t st) {
+    // K_j, V_j (smem, SW128 K-major) -> TMEM A-operand layout (16 elements per 8 columns)
+    auto copy_kv = [&](uint32_t kvb) {
       const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
-      const uint32_t qa = q_base + st * C::kTileBytes, da = do_base + st * C::kTileBytes;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        sm100::tmem_cp_128x256b(tmem + C::kColK + kk * 8, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024));
+        sm100::tmem_cp_128x256b(tmem + C::kColV + kk * 8, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024));
+      }
+    };
+    // S^T_q = K Q_q^T and dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; A from TMEM)
+    auto mma1 = [&](uint32_t st, uint32_t q) {
+      const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
-        sm100::mma_ss(tmem + C::kColS, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024),
+        sm100::mma_ts(tmem + C::kColS + q * 64, tmem + C::kColK + kk * 8,
                       sm100::make_sdesc_sw128(qa + kk * 32, 16, 1024), idesc_s, kk > 0);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
-        sm100::mma_ss(tmem + C::kColDP, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024),
+        sm100::mma_ts(tmem + C::kColDP + q * 64, tmem + C::kColV + kk * 8,
                       sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_s, kk > 0);
-      sm100::mma_commit(s_full);
+      sm100::mma_commit(&s_full[q]);
+    };
+    // dV += P^T_q dO_q ; dK += dS^T_q Q_q   (M = keys, N = d, K = 64 queries; A from TMEM)
+    auto mma2 = [&](uint32_t st, uint32_t q, bool first) {
+      const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        // queries [64q + 16kk, +16): warpgroup 2q + kk/2 packed them at its S cols + 8 (kk & 1)
+        const uint32_t a_col = (2 * q + (kk >> 1)) * 32 + (kk & 1) * 8;
+        sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + a_col,
+                      sm100::make_sdesc_sw128(da + kk * 2048, kTile * 128, 1024), idesc_acc,
+                      (first && kk == 0) ? 0u : 1u);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t a_col = (2 * q + (kk >> 1)) * 32 + (kk & 1) * 8;
+        sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + a_col,
+                      sm100::make_sdesc_sw128(qa + kk * 2048, kTile * 128, 1024), idesc_acc,
+                      (first && kk == 0) ? 0u : 1u);
+      }
     };
 
     TileIter cur;
@@ -249,7 +276,11 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_wait(&kv_full[cur.item_c & 1], (cur.item_c >> 1) & 1);
       sm100::mbar_wait(&qdo_full[0], 0);
       sm100::tc_fence_after();
-      if (sm100::elect_one()) mma_s(cur.item_c & 1, 0);
+      if (sm100::elect_one()) {
+        copy_kv(cur.item_c & 1);
+        mma1(0, 0);
+        mma1(0, 1);
+      }
       __syncwarp();
     }
     uint32_t t = 0;
@@ -257,43 +288,38 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       TileIter nxt = cur;
       nxt.advance(args.items);
       const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1, buf = t & 1;
-      sm100::mbar_wait(p_full, t & 1);                 // S^T/dP^T(t) consumed; P^T(t), dS^T(t) written
+      const uint32_t st1 = (t + 1) % C::kQStages;
+      // long wait (a compute phase): poll with back-off so the MMA warp does not steal issue slots
+      sm100::mbar_wait_backoff(&p_full[0], t & 1);
       if (lane == 0) sm100::trace_event(args.trace, 0 * 512 + t, 0 * 512 + 512);
-      if (nxt.valid) {                                 // next tile's scores first: the compute warps
-        const uint32_t st1 = (t + 1) % C::kQStages;   // start on them while dV/dK/dQ(t) run
+      if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);   // epilogue read previous dV/dK
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
+      __syncwarp();
+      if (nxt.valid) {
         if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
         sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
         sm100::tc_fence_after();
-        if (sm100::elect_one()) mma_s(nxt.item_c & 1, st1);
+        if (sm100::elect_one()) {
+          // the copy executes after every earlier MMA (tcgen05 ops of one thread run in order), so
+          // S/dP(i, q1) has finished reading the previous K/V columns
+          if (nxt.i == 0) copy_kv(nxt.item_c & 1);
+          mma1(st1, 0);
+        }
         __syncwarp();
       }
       if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
-      if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);   // epilogue read previous dV/dK
+      sm100::mbar_wait_backoff(&p_full[1], t & 1);
+      if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
       sm100::tc_fence_after();
       if (sm100::elect_one()) {
-        const bool first = cur.i == 0;
-        const uint32_t qa = q_base + st * C::kTileBytes, da = do_base + st * C::kTileBytes;
-        const uint32_t dsa = ds_base + buf * C::kDSBytes;
-        // dV += P^T dO   (M = keys, N = d, K = 128 queries)
-#pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk)
-          sm100::mma_ts(tmem + C::kColDV, tmem + C::kColP + kk * 8,
-                        sm100::make_sdesc_sw128(da + kk * 2048, kTile * 128, 1024), idesc_dv,
-                        (first && kk == 0) ? 0u : 1u);
-        sm100::mma_commit(p_free);
-        // dK += dS^T Q   (A = dS^T K-major: queries [64h, 64h+64) of each key row live in half h)
-#pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk)
-          sm100::mma_ss(tmem + C::kColDK,
-                        sm100::make_sdesc_sw128(dsa + (kk >> 2) * (kTile * 128) + (kk & 3) * 32, 16, 1024),
-                        sm100::make_sdesc_sw128(qa + kk * 2048, kTile * 128, 1024), idesc_dk,
-                        (first && kk == 0) ? 0u : 1u);
-        sm100::mma_commit(&qdo_empty[st]);             // last readers of Q_i, dO_i
-        if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);
+        mma2(st, 1, false);
+        sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
+        if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
+        if (nxt.valid) mma1(st1, 1);
       }
       __syncwarp();
-      if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
-      sm100::mbar_wait(dq_empty, (t & 1) ^ 1);         // epilogue drained dQ(t-1)
+      sm100::mbar_wait(dq_empty, (t & 1) ^ 1);                   // epilogue drained dQ(t-1)
       sm100::tc_fence_after();
       if (sm100::elect_one()) {
         const uint32_t ka = k_base + kvb * C::kTileBytes;
@@ -305,7 +331,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                         sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024), idesc_dq, kk > 0);
         sm100::mma_commit(&ds_free[buf]);
         sm100::mma_commit(dq_full);
-        if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);
+        if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);   // K/V smem slot free
       }
       __syncwarp();
       if (lane == 0) sm100::trace_event(args.trace, 3 * 512 + t, 3 * 512 + 512);
@@ -313,15 +339,16 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       ++t;
     }
   } else if (warp < kComputeWarps) {
-    // ===================== compute warpgroups (queries [32g, 32g + 32)) =====================
-    const uint32_t g = warp >> 2;
+    // ===================== compute warpgroups (queries [32w, 32w + 32), half w / 2) =====================
+    const uint32_t w4 = warp >> 2;                     // warpgroup
+    const uint32_t qh = w4 >> 1;                       // query half
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
-    const uint32_t s_col = C::kColS + g * 32, dp_col = C::kColDP + g * 32, p_col = C::kColP + g * 16;
-    // dS^T smem: query half (g >> 1), 16-byte chunks (g & 1) * 4 + [0, 4) of the 128-byte row
+    const uint32_t s_col = C::kColS + w4 * 32, dp_col = C::kColDP + w4 * 32;
+    // dS^T smem: query half qh, 16-byte chunks (w4 & 1) * 4 + [0, 4) of the 128-byte row
     const uint32_t ds_row =
-        sm100::smem_u32(smem + C::kDSOff + (g >> 1) * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128);
+        sm100::smem_u32(smem + C::kDSOff + qh * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128);
     uint32_t t = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
@@ -335,11 +362,13 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       for (int i = 0; i < nqt; ++i, ++t) {
-        sm100::mbar_wait(s_full, t & 1);
+        sm100::mbar_wait(&s_full[qh], t & 1);
         if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 4 * 512 + t, 5 * 512);
+        if (lane == 0 && warp == 8) sm100::trace_event(args.trace, 6 * 512 + t, 7 * 512);
+        sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) done with this dS buffer
         sm100::tc_fence_after();
         const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
-        const int q0 = i * kTile + (int)g * 32;
+        const int q0 = i * kTile + (int)w4 * 32;
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {   // 16 query columns per step (register budget)
           float s[16], dp[16];
@@ -353,15 +382,12 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           uint32_t pp[8], dd[8];
           if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16);
           else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
-          if (ch == 0) {
-            sm100::mbar_wait(p_free, (t & 1) ^ 1);                   // dV(t-1) finished reading P^T
-            sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dK/dQ(t-2) done with this buffer
-            sm100::tc_fence_after();
-          }
-          sm100::tmem_st8(tmem + lane_addr + p_col + ch * 8, pp);
+          // P^T / dS^T over the first half of this warpgroup's own (already read) columns
+          sm100::tmem_st8(tmem + lane_addr + s_col + ch * 8, pp);
+          sm100::tmem_st8(tmem + lane_addr + dp_col + ch * 8, dd);
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const uint32_t chunk = (uint32_t)((g & 1) * 4 + ch * 2 + u) ^ (row & 7);
+            const uint32_t chunk = (uint32_t)((w4 & 1) * 4 + ch * 2 + u) ^ (row & 7);
             sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
           }
         }
@@ -369,8 +395,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(p_full);
+        if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
         if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 5 * 512 + t, 6 * 512);
+        if (lane == 0 && warp == 8) sm100::trace_event(args.trace, 7 * 512 + t, 8 * 512);
       }
     }
   } else if (warp < C::kWarpTMA) {
@@ -389,7 +416,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const size_t zh = (size_t)(b * args.H + h);
       for (int i = 0; i < nqt; ++i, ++t) {
         sm100::mbar_wait_backoff(dq_full, t & 1);
-        if (lane == 0 && quarter == 0) sm100::trace_event(args.trace, 6 * 512 + t, 7 * 512);
         sm100::tc_fence_after();
         const int q = i * kTile + (int)row;
         float* dst = args.dq_acc + (zh * args.Nq + q) * D;

@@ -222,7 +222,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       for (int j = 0; j < nkt; ++j) {
         if (j + 2 < nkt) issue_s(kv_it + j + 2, s_it + j + 2);
         const uint32_t si = s_it + j;
-        sm100::mbar_wait(&p_full[si % C::kSBuf], (si / C::kSBuf) & 1);
+        sm100::mbar_wait_backoff(&p_full[si % C::kSBuf], (si / C::kSBuf) & 1);
         if (j == 0) sm100::mbar_wait(o_empty, (c & 1) ^ 1);   // epilogue drained the previous O
         const uint32_t kvi = kv_it + j;
         const uint32_t st = kvi % C::kStages;
