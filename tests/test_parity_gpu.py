@@ -222,3 +222,56 @@ def test_sigmoid_slow_and_saturated_paths(bias, scale):
     for name, got, ref in (("o", o, ro), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
         err = relerr(f64(got), ref)
         assert err <= BF16_TOL, f"{name} rel err {err} (bias={bias}, scale={scale})"
+
+
+def test_cp_backward_partials_sum():
+    """Key-split backward: per-block fp32 dQ partials (DQ_F32_PARTIAL) sum to dQ; dK/dV blocks are
+    the unsplit dK/dV rows (keys are owned) -- the CP exchange of SURVEY 8e, simulated on one GPU."""
+    sa = _sa()
+    cfg = I.Config("cpb", B=2, H=2, N=512, d=64, lengths=[512, 300], seed=16)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    b = -math.log(512)
+    G, blk = 4, 128
+    dq_sum = torch.zeros(q.shape, dtype=torch.float32, device="cuda")
+    dks, dvs = [], []
+    for r in range(G):
+        ks, vs = (t[:, :, r * blk:(r + 1) * blk].contiguous() for t in (k, v))
+        nk_r = torch.clamp(nk - r * blk, 0, blk).to(torch.int32)
+        dq_r, dk_r, dv_r = sa.sigattn_bwd(q, ks, vs, do, nq, nk_r, None, b, dq_f32=True)
+        assert dq_r.dtype == torch.float32
+        dq_sum += dq_r
+        dks.append(dk_r)
+        dvs.append(dv_r)
+    bias = np.full(2, b)
+    rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, 1 / 8, bias)
+    assert relerr(f64(dq_sum), rdq) <= BF16_TOL
+    assert relerr(f64(torch.cat(dks, 2)), rdk) <= BF16_TOL
+    assert relerr(f64(torch.cat(dvs, 2)), rdv) <= BF16_TOL
+
+
+def test_cp_autograd_world1_nccl():
+    """cp_sigmoid_attention through torch.distributed (NCCL, world 1) + autograd."""
+    import os
+    import torch.distributed as dist
+    from paper_2604_27124_b200 import parallel as par
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29641")
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1)
+        created = True
+    try:
+        cfg = I.Config("cpw1", B=1, H=2, N=256, d=64, seed=17)
+        q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+        qq, kk, vv = (t.clone().requires_grad_(True) for t in (q, k, v))
+        o = par.cp_sigmoid_attention(qq, kk, vv, par.CPShard(0, 1, 256))
+        o.backward(do)
+        b = np.full(1, -math.log(256))
+        ro = oracle.fwd(f64(q), f64(k), f64(v), [256], [256], 1 / 8, b)
+        rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), [256], [256], 1 / 8, b)
+        assert relerr(f64(o), ro) <= BF16_TOL
+        for got, ref in ((qq.grad, rdq), (kk.grad, rdk), (vv.grad, rdv)):
+            assert relerr(f64(got), ref) <= BF16_TOL
+    finally:
+        if created:
+            dist.destroy_process_group()
