@@ -15,13 +15,13 @@
 // credited 10 d per (query, key) pair.
 //
 // Pipelining: the MMA warp issues, per tile i,   dV/dK(i, q0) | S,dP(i+1, q0) | dV/dK(i, q1) |
-// S,dP(i+1, q1) | dQ(i)   so the half-0 warps compute tile i+1 while the half-1 warps still
-// compute tile i, and the tensor core always has the other half's work queued.
+// S,dP(i+1, q1) | dQ(i)   so while the compute warps work on one half, the tensor core finishes the
+// other half and prepares the next tile's scores for it.
 //
 // CTA roles (768 threads, persistent, one CTA per SM; single-thread roles in the highest warp ids,
 // which the warp scheduler favours):
-//   warps 0-15  four compute warpgroups; thread = key row (TMEM lane); WG w = queries [32w, 32w+32),
-//               i.e. WGs 0,1 form query half 0 and WGs 2,3 half 1
+//   warps 0-15  compute: thread = key row (TMEM lane); all 16 warps process query half 0, then half 1;
+//               warpgroup w takes 16 queries [64q + 16w, +16) of half q
 //   warps 16-19 epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
 //               dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
 //   warp 20     TMA: K_j, V_j (2 slots), Q_i + dO_i (3 stages)
@@ -162,7 +162,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&kv_empty[i], 1);
       sm100::mbar_init(&ds_free[i], 1);
       sm100::mbar_init(&s_full[i], 1);
-      sm100::mbar_init(&p_full[i], kComputeWarps / 2);   // the 8 warps of one query half
+      sm100::mbar_init(&p_full[i], kComputeWarps);       // every compute warp works on every half
     }
     for (int i = 0; i < C::kQStages; ++i) {
       sm100::mbar_init(&qdo_full[i], 1);
@@ -185,6 +185,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (threadIdx.x == 0) sm100::trace_globaltime(args.trace, 4094);
   const int n_items = *args.n_items;
 
   if (warp == C::kWarpTMA) {
@@ -255,15 +256,15 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        // queries [64q + 16kk, +16): warpgroup 2q + kk/2 packed them at its S cols + 8 (kk & 1)
-        const uint32_t a_col = (2 * q + (kk >> 1)) * 32 + (kk & 1) * 8;
+        // queries [64q + 16kk, +16): warpgroup kk packed them at S cols 64q + 16kk + [0, 8)
+        const uint32_t a_col = q * 64 + kk * 16;
         sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + a_col,
                       sm100::make_sdesc_sw128(da + kk * 2048, kTile * 128, 1024), idesc_acc,
                       (first && kk == 0) ? 0u : 1u);
       }
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const uint32_t a_col = (2 * q + (kk >> 1)) * 32 + (kk & 1) * 8;
+        const uint32_t a_col = q * 64 + kk * 16;
         sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + a_col,
                       sm100::make_sdesc_sw128(qa + kk * 2048, kTile * 128, 1024), idesc_acc,
                       (first && kk == 0) ? 0u : 1u);
@@ -339,16 +340,13 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       ++t;
     }
   } else if (warp < kComputeWarps) {
-    // ===================== compute warpgroups (queries [32w, 32w + 32), half w / 2) =====================
-    const uint32_t w4 = warp >> 2;                     // warpgroup
-    const uint32_t qh = w4 >> 1;                       // query half
+    // ===================== compute warps: all 16 work on each query half in turn =====================
+    // warpgroup w4 owns queries [16 w4, 16 w4 + 16) of each 64-query half
+    const uint32_t w4 = warp >> 2;
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
-    const uint32_t s_col = C::kColS + w4 * 32, dp_col = C::kColDP + w4 * 32;
-    // dS^T smem: query half qh, 16-byte chunks (w4 & 1) * 4 + [0, 4) of the 128-byte row
-    const uint32_t ds_row =
-        sm100::smem_u32(smem + C::kDSOff + qh * (kTile * 128) + (row >> 3) * 1024 + (row & 7) * 128);
+    const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
     uint32_t t = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
@@ -362,42 +360,47 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       for (int i = 0; i < nqt; ++i, ++t) {
-        sm100::mbar_wait(&s_full[qh], t & 1);
-        if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 4 * 512 + t, 5 * 512);
-        if (lane == 0 && warp == 8) sm100::trace_event(args.trace, 6 * 512 + t, 7 * 512);
-        sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) done with this dS buffer
-        sm100::tc_fence_after();
         const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
-        const int q0 = i * kTile + (int)w4 * 32;
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {   // 16 query columns per step (register budget)
+        for (int qh = 0; qh < 2; ++qh) {
+          sm100::mbar_wait(&s_full[qh], t & 1);
+#define BWD_TR(e) if (lane == 0 && t >= 8 && t < 16) sm100::trace_event(args.trace, 4 * 512 + (warp * 8 + (t - 8)) * 8 + (e), 6 * 512)
+          if (qh == 0) BWD_TR(0);
+          if (qh == 0) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) done with it
+          sm100::tc_fence_after();
+          const uint32_t s_col = C::kColS + qh * 64 + w4 * 16, dp_col = C::kColDP + qh * 64 + w4 * 16;
           float s[16], dp[16];
-          sm100::tmem_ld16(tmem + lane_addr + s_col + ch * 16, s);
-          sm100::tmem_ld16(tmem + lane_addr + dp_col + ch * 16, dp);
+          sm100::tmem_ld16(tmem + lane_addr + s_col, s);
+          sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
           sm100::tmem_wait_ld_dep16(s);
           sm100::tmem_wait_ld_dep16(dp);
-          // valid query columns in this step; the masked variant is chosen warp-uniformly (it also
-          // zeroes the rows of padded keys)
-          const int ncol = nq - (q0 + ch * 16);
+          // valid query columns here; the masked variant is chosen warp-uniformly (it also zeroes the
+          // rows of padded keys)
+          const int ncol = nq - (i * kTile + qh * 64 + (int)w4 * 16);
           uint32_t pp[8], dd[8];
           if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16);
           else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
-          // P^T / dS^T over the first half of this warpgroup's own (already read) columns
-          sm100::tmem_st8(tmem + lane_addr + s_col + ch * 8, pp);
-          sm100::tmem_st8(tmem + lane_addr + dp_col + ch * 8, dd);
+          BWD_TR(qh == 0 ? 1 : 4);
+          // P^T / dS^T over the first half of this warp's own (already read) columns
+          sm100::tmem_st8(tmem + lane_addr + s_col, pp);
+          sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
+          if (qh == 1) BWD_TR(5);
+          // dS^T into the swizzled smem tile: half qh, 16 queries = 16-byte chunks 2 w4, 2 w4 + 1
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const uint32_t chunk = (uint32_t)((w4 & 1) * 4 + ch * 2 + u) ^ (row & 7);
-            sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+            const uint32_t chunk = (uint32_t)(w4 * 2 + u) ^ (row & 7);
+            sm100::st_shared_v4(dsr + qh * (kTile * 128) + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2],
+                                dd[4 * u + 3]);
           }
+          sm100::tmem_wait_st();
+          BWD_TR(qh == 0 ? 2 : 6);
+          sm100::fence_proxy_async_smem();
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
+          BWD_TR(qh == 0 ? 3 : 7);
+#undef BWD_TR
         }
-        sm100::tmem_wait_st();
-        sm100::fence_proxy_async_smem();
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
-        if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 5 * 512 + t, 6 * 512);
-        if (lane == 0 && warp == 8) sm100::trace_event(args.trace, 7 * 512 + t, 8 * 512);
       }
     }
   } else if (warp < C::kWarpTMA) {
@@ -485,6 +488,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 
   sm100::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) sm100::trace_globaltime(args.trace, 4095);
   if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);
 }
 

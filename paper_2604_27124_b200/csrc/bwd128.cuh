@@ -1,0 +1,361 @@
+// bwd128.cuh -- sm_100a backward kernel for head dimension d = 128 (same method as bwd.cuh).
+//
+// With d = 128 the d-wide accumulators dV, dK (128 TMEM columns each) leave no room for full
+// 128x128 score tiles, so each key tile (128 keys, owned by the CTA; K_j, V_j resident in smem)
+// loops over 64-query tiles i and dQ is produced transposed (M = d) so that it needs only 64
+// columns:
+//     S^T  = K_j Q_i^T,   dP^T = V_j dO_i^T          SS, M = 128 keys, N = 64 queries, K = d
+//     P^T  = mask . sigma(alpha S^T + b),  dS^T = P^T (1 - P^T) dP^T
+//     dV_j += P^T dO_i,   dK_j += dS^T Q_i           TS (P^T, dS^T in TMEM), N = d = 128
+//     dQ_i^T = K_j^T dS_i^T                          SS, M = d, N = 64 queries, K = keys
+//                                                    (A = K read MN-major, B = dS^T smem MN-major)
+// dQ^T is drained lane = d index and reduce-added (coalesced over d) into the fp32 workspace; alpha
+// is applied in the epilogues.  MMA order per tile: dV/dK(i) | S,dP(i+1) | dQ(i), so
+// the compute warps start on tile i+1 while dQ(i) runs.
+// Roles as in bwd.cuh (768 threads): warps 0-15 compute (warpgroup w: queries [16w, 16w+16) of the
+// 64-query tile), 16-19 epilogue, 20 TMA, 21 MMA, 22 TMEM allocator.
+// TMEM: S^T [0,64) dP^T [64,128) dV [128,256) dK [256,384) dQ^T [384,448).
+// Shared memory: K, V (single slot, 2 x 32 KB), Q_i + dO_i ring (3 x 2 x 16 KB), dS^T (2 x 16 KB).
+#pragma once
+#include "bwd.cuh"
+
+namespace sigattn {
+
+struct Bwd128Cfg {
+  static constexpr int D = 128;
+  static constexpr int kQT = 64;                             // queries per tile
+  static constexpr int kKVBytes = kTile * D * 2;             // 32 KB: [128 keys][2 x 64 d]
+  static constexpr int kQBytes = kQT * D * 2;                // 16 KB: [64 q][2 x 64 d]
+  static constexpr int kQStages = 3;
+  static constexpr int kKOff = 0;
+  static constexpr int kVOff = kKOff + kKVBytes;
+  static constexpr int kQOff = kVOff + kKVBytes;
+  static constexpr int kDOOff = kQOff + kQStages * kQBytes;
+  static constexpr int kDSOff = kDOOff + kQStages * kQBytes;
+  static constexpr int kDSBytes = kTile * 128;               // [128 keys][64 q] 16-bit = 16 KB
+  static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
+  static constexpr int kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 1;
+  static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
+  static constexpr int kWarpEpi = 16, kWarpTMA = 20, kWarpMMA = 21, kWarpAlloc = 22;
+  static constexpr int kThreads = 768;
+  static constexpr uint32_t kTmemCols = 512;
+  static constexpr uint32_t kColS = 0, kColDP = 64, kColDV = 128, kColDK = 256, kColDQ = 384;
+};
+
+template <bool kBf16>
+__global__ void __launch_bounds__(Bwd128Cfg::kThreads, 1)
+sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                      const BwdArgs args) {
+  using C = Bwd128Cfg;
+  constexpr int D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* kv_empty = bars + 1;
+  uint64_t* qdo_full = bars + 2;                  // [kQStages]
+  uint64_t* qdo_empty = qdo_full + C::kQStages;
+  uint64_t* s_full = qdo_empty + C::kQStages;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* ds_free = p_full + 1;                 // [2]
+  uint64_t* dq_full = ds_free + 2;
+  uint64_t* dq_empty = dq_full + 1;
+  uint64_t* acc_full = dq_empty + 1;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+
+  const uint32_t warp = sm100::warp_id();
+  const uint32_t lane = sm100::lane_id();
+
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(kv_full, 1);
+    sm100::mbar_init(kv_empty, 1);
+    for (int i = 0; i < C::kQStages; ++i) {
+      sm100::mbar_init(&qdo_full[i], 1);
+      sm100::mbar_init(&qdo_empty[i], 1);
+    }
+    sm100::mbar_init(s_full, 1);
+    sm100::mbar_init(p_full, 16);
+    sm100::mbar_init(&ds_free[0], 1);
+    sm100::mbar_init(&ds_free[1], 1);
+    sm100::mbar_init(dq_full, 1);
+    sm100::mbar_init(dq_empty, 4);
+    sm100::mbar_init(acc_full, 1);
+    sm100::mbar_init(acc_empty, 4);
+    sm100::fence_barrier_init();
+  }
+  if (warp == C::kWarpTMA && lane == 0) {
+    sm100::tma_prefetch_desc(&tmQ);
+    sm100::tma_prefetch_desc(&tmK);
+    sm100::tma_prefetch_desc(&tmV);
+    sm100::tma_prefetch_desc(&tmDO);
+  }
+  if (warp == C::kWarpAlloc) sm100::tmem_alloc<C::kTmemCols>(tmem_holder);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int n_items = *args.n_items;
+  auto item_tiles = [&](int b) {   // 64-query tiles of sequence b
+    const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
+    return (nq + C::kQT - 1) / C::kQT;
+  };
+
+  if (warp == C::kWarpTMA) {
+    // ===================== TMA producer =====================
+    const uint64_t pol_kv = sm100::policy_evict_first();
+    const uint64_t pol_q = sm100::policy_evict_last();
+    uint32_t kv_c = 0, t = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      if (item.w <= 0) continue;
+      const int b = item.x, h = item.y, kt = item.z, nqt = item_tiles(b);
+      const int zh = b * args.H + h;
+      sm100::mbar_wait_backoff(kv_empty, (kv_c & 1) ^ 1);
+      if (sm100::elect_one()) {
+        sm100::mbar_arrive_expect_tx(kv_full, 2 * C::kKVBytes);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          sm100::tma_load_3d(smem + C::kKOff + s * (kTile * 128), &tmK, kv_full, s * 64, kt * kTile, zh, pol_kv);
+          sm100::tma_load_3d(smem + C::kVOff + s * (kTile * 128), &tmV, kv_full, s * 64, kt * kTile, zh, pol_kv);
+        }
+      }
+      __syncwarp();
+      for (int i = 0; i < nqt; ++i, ++t) {
+        const uint32_t st = t % C::kQStages;
+        sm100::mbar_wait_backoff(&qdo_empty[st], ((t / C::kQStages) & 1) ^ 1);
+        if (sm100::elect_one()) {
+          sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kQBytes);
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            sm100::tma_load_3d(smem + C::kQOff + st * C::kQBytes + s * (C::kQT * 128), &tmQ, &qdo_full[st], s * 64,
+                               i * C::kQT, zh, pol_q);
+            sm100::tma_load_3d(smem + C::kDOOff + st * C::kQBytes + s * (C::kQT * 128), &tmDO, &qdo_full[st],
+                               s * 64, i * C::kQT, zh, pol_q);
+          }
+        }
+        __syncwarp();
+      }
+      ++kv_c;
+    }
+  } else if (warp == C::kWarpMMA) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, C::kQT, false, false);   // S^T, dP^T
+    constexpr uint32_t idesc_acc = sm100::make_idesc_f16(kBf16, 128, D, false, true);       // dV, dK
+    constexpr uint32_t idesc_dq = sm100::make_idesc_f16(kBf16, 128, C::kQT, true, true);    // dQ^T
+    const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
+    const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
+    const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
+    const uint32_t do_base = sm100::smem_u32(smem + C::kDOOff);
+    const uint32_t ds_base = sm100::smem_u32(smem + C::kDSOff);
+    auto mma_s = [&](uint32_t st) {
+      const uint32_t qa = q_base + st * C::kQBytes, da = do_base + st * C::kQBytes;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t ko = (kk >> 2) * (kTile * 128) + (kk & 3) * 32, qo = (kk >> 2) * (C::kQT * 128) + (kk & 3) * 32;
+        sm100::mma_ss(tmem + C::kColS, sm100::make_sdesc_sw128(k_base + ko, 16, 1024),
+                      sm100::make_sdesc_sw128(qa + qo, 16, 1024), idesc_s, kk > 0);
+      }
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t ko = (kk >> 2) * (kTile * 128) + (kk & 3) * 32, qo = (kk >> 2) * (C::kQT * 128) + (kk & 3) * 32;
+        sm100::mma_ss(tmem + C::kColDP, sm100::make_sdesc_sw128(v_base + ko, 16, 1024),
+                      sm100::make_sdesc_sw128(da + qo, 16, 1024), idesc_s, kk > 0);
+      }
+      sm100::mma_commit(s_full);
+    };
+    auto mma_dq = [&](uint32_t buf) {
+      const uint32_t dsa = ds_base + buf * C::kDSBytes;
+      // dQ^T = K^T dS^T: A = K read MN-major (M = d: 64-wide atoms at LBO = 16 KB), B = dS^T MN-major
+#pragma unroll
+      for (int kk = 0; kk < kTile / 16; ++kk)
+        sm100::mma_ss(tmem + C::kColDQ, sm100::make_sdesc_sw128(k_base + kk * 2048, kTile * 128, 1024),
+                      sm100::make_sdesc_sw128(dsa + kk * 2048, 16, 1024), idesc_dq, kk > 0);
+    };
+
+    uint32_t t = 0, item_c = 0;
+    bool primed = false;   // S/dP of the current tile already issued
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      if (item.w <= 0) continue;
+      const int nqt = item_tiles(item.x);
+      sm100::mbar_wait(kv_full, item_c & 1);
+      if (!primed) {
+        sm100::mbar_wait(&qdo_full[t % C::kQStages], (t / C::kQStages) & 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) mma_s(t % C::kQStages);
+        __syncwarp();
+      }
+      for (int i = 0; i < nqt; ++i, ++t) {
+        const uint32_t st = t % C::kQStages, buf = t & 1;
+        sm100::mbar_wait_backoff(p_full, t & 1);
+        if (i == 0) sm100::mbar_wait(acc_empty, (item_c & 1) ^ 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint32_t qa = q_base + st * C::kQBytes, da = do_base + st * C::kQBytes;
+#pragma unroll
+          for (int kk = 0; kk < C::kQT / 16; ++kk)   // dV += P^T dO  (queries 16kk: warpgroup kk's columns)
+            sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + kk * 16,
+                          sm100::make_sdesc_sw128(da + kk * 2048, C::kQT * 128, 1024), idesc_acc,
+                          (i == 0 && kk == 0) ? 0u : 1u);
+#pragma unroll
+          for (int kk = 0; kk < C::kQT / 16; ++kk)   // dK += dS^T Q
+            sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + kk * 16,
+                          sm100::make_sdesc_sw128(qa + kk * 2048, C::kQT * 128, 1024), idesc_acc,
+                          (i == 0 && kk == 0) ? 0u : 1u);
+          sm100::mma_commit(&qdo_empty[st]);
+          if (i == nqt - 1) sm100::mma_commit(acc_full);
+        }
+        __syncwarp();
+        const bool has_next_here = i + 1 < nqt;
+        if (has_next_here) {     // next tile's scores before dQ(i)
+          const uint32_t st1 = (t + 1) % C::kQStages;
+          sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
+          sm100::tc_fence_after();
+          if (sm100::elect_one()) mma_s(st1);
+          __syncwarp();
+        }
+        sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          mma_dq(buf);
+          sm100::mma_commit(&ds_free[buf]);
+          sm100::mma_commit(dq_full);
+          if (i == nqt - 1) sm100::mma_commit(kv_empty);
+        }
+        __syncwarp();
+      }
+      primed = false;   // the next item's K/V arrive only after this item's last dQ (single K/V slot)
+      ++item_c;
+    }
+  } else if (warp < C::kWarpEpi) {
+    // ===================== compute warps: warpgroup w4 = queries [16 w4, 16 w4 + 16) =====================
+    const uint32_t w4 = warp >> 2;
+    const uint32_t quarter = warp & 3;
+    const uint32_t row = quarter * 32 + lane;
+    const uint32_t lane_addr = (quarter * 32) << 16;
+    const uint32_t s_col = C::kColS + w4 * 16, dp_col = C::kColDP + w4 * 16;
+    const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
+    uint32_t t = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      if (item.w <= 0) continue;
+      const int b = item.x, kt = item.z, nqt = item_tiles(b);
+      const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
+      const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
+      const float bias = args.bias_per_seq ? args.bias_per_seq[b] : args.bias;
+      const float a2 = args.scale * kLog2e;
+      const float b2 = bias * kLog2e;
+      const bool key_valid = kt * kTile + (int)row < nk;
+      const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
+      for (int i = 0; i < nqt; ++i, ++t) {
+        sm100::mbar_wait(s_full, t & 1);
+        sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
+        sm100::tc_fence_after();
+        float s[16], dp[16];
+        sm100::tmem_ld16(tmem + lane_addr + s_col, s);
+        sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
+        sm100::tmem_wait_ld_dep16(s);
+        sm100::tmem_wait_ld_dep16(dp);
+        const int ncol = nq - (i * C::kQT + (int)w4 * 16);
+        uint32_t pp[8], dd[8];
+        if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16);
+        else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
+        sm100::tmem_st8(tmem + lane_addr + s_col, pp);
+        sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
+        const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t chunk = (uint32_t)(w4 * 2 + u) ^ (row & 7);
+          sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+        }
+        sm100::tmem_wait_st();
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(p_full);
+      }
+    }
+  } else if (warp < C::kWarpTMA) {
+    // ===================== epilogue: dQ^T drain (lane = d index) + dK/dV =====================
+    const uint32_t quarter = warp & 3;
+    const uint32_t row = quarter * 32 + lane;          // d index for dQ^T, key row for dK/dV
+    const uint32_t lane_addr = (quarter * 32) << 16;
+    const float alpha = args.scale;
+    uint32_t t = 0, item_c = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      if (item.w <= 0) continue;
+      const int b = item.x, h = item.y, kt = item.z, nqt = item_tiles(b);
+      const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
+      const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
+      const size_t zh = (size_t)(b * args.H + h);
+      for (int i = 0; i < nqt; ++i, ++t) {
+        sm100::mbar_wait_backoff(dq_full, t & 1);
+        sm100::tc_fence_after();
+        float r[4][16];
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + c4 * 16, r[c4]);
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) sm100::tmem_wait_ld_dep16(r[c4]);
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(dq_empty);
+        float* base = args.dq_acc + (zh * args.Nq + (size_t)i * C::kQT) * D + row;
+        const int nrow = nq - i * C::kQT;
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int q = c4 * 16 + e;
+            if (q < nrow) atomicAdd(base + (size_t)q * D, alpha * r[c4][e]);   // coalesced over d
+          }
+      }
+      sm100::mbar_wait_backoff(acc_full, item_c & 1);
+      sm100::tc_fence_after();
+      const int key = kt * kTile + (int)row;
+      const bool key_valid = key < nk;
+      const size_t off = (zh * args.Nk + key) * D;
+#pragma unroll 1
+      for (int which = 0; which < 2; ++which) {
+        const uint32_t col0 = which == 0 ? C::kColDV : C::kColDK;
+        const float sc = which == 0 ? 1.0f : alpha;
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(which == 0 ? args.dv : args.dk) + off);
+#pragma unroll 1
+        for (int hh = 0; hh < 4; ++hh) {
+          float r[2][16];
+          sm100::tmem_ld16(tmem + lane_addr + col0 + hh * 32, r[0]);
+          sm100::tmem_ld16(tmem + lane_addr + col0 + hh * 32 + 16, r[1]);
+          sm100::tmem_wait_ld_dep16(r[0]);
+          sm100::tmem_wait_ld_dep16(r[1]);
+          if (which == 1 && hh == 3) {
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(acc_empty);
+          }
+          if (key < args.Nk) {
+#pragma unroll
+            for (int c4 = 0; c4 < 2; ++c4)
+#pragma unroll
+              for (int e = 0; e < 16; e += 8) {
+                uint4 w;
+                w.x = key_valid ? sm100::pack2<kBf16>(sc * r[c4][e], sc * r[c4][e + 1]) : 0u;
+                w.y = key_valid ? sm100::pack2<kBf16>(sc * r[c4][e + 2], sc * r[c4][e + 3]) : 0u;
+                w.z = key_valid ? sm100::pack2<kBf16>(sc * r[c4][e + 4], sc * r[c4][e + 5]) : 0u;
+                w.w = key_valid ? sm100::pack2<kBf16>(sc * r[c4][e + 6], sc * r[c4][e + 7]) : 0u;
+                dst[hh * 4 + c4 * 2 + (e >> 3)] = w;
+              }
+          }
+        }
+      }
+      ++item_c;
+    }
+  }
+
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+}
+
+}  // namespace sigattn

@@ -130,6 +130,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (threadIdx.x == 0) sm100::trace_globaltime(args.trace, 4094);
 
   const int n_items = *args.n_items;
   const int BH = args.B * args.H;
@@ -338,6 +339,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 
   sm100::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) sm100::trace_globaltime(args.trace, 4095);
   if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);
 }
 

@@ -15,6 +15,7 @@
 
 #include "../../include/sigattn.h"
 #include "bwd.cuh"
+#include "bwd128.cuh"
 #include "fwd.cuh"
 #include "sched.cuh"
 
@@ -67,12 +68,12 @@ EncodeTiledFn get_encode() {
 // 128-byte swizzle: exactly the UMMA K-major / MN-major SWIZZLE_128B atom.  Rows past `rows`
 // read as zero (OOB fill), so a ragged last tile never touches another head's data.
 sigattn_status make_tmap(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int elem_bytes, int d, int rows,
-                         int bh) {
+                         int bh, int box_rows = 128) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(SIGATTN_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)bh};
   cuuint64_t strides[2] = {(cuuint64_t)d * elem_bytes, (cuuint64_t)d * elem_bytes * rows};
-  cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), 128, 1};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -205,6 +206,45 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);
   kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
+  prof_record(3, s);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+template <bool kBf16>
+sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
+                             float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
+                             cudaStream_t s) {
+  const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tq, tk, tv, tdo;
+  const int bh = p->B * p->H;
+  sigattn_status st;
+  if ((st = make_tmap(&tq, q, dt, 2, 128, p->Nq, bh, Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tk, k, dt, 2, 128, p->Nk, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tv, v, dt, 2, 128, p->Nk, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tdo, dout, dt, 2, 128, p->Nq, bh, Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
+  BwdArgs a;
+  a.items = items;
+  a.n_items = n_items;
+  a.seqlens_q = p->seqlens_q;
+  a.seqlens_k = p->seqlens_k;
+  a.bias_per_seq = p->bias_per_seq;
+  a.bias = p->bias;
+  a.scale = p->scale;
+  a.B = p->B;
+  a.H = p->H;
+  a.Nq = p->Nq;
+  a.Nk = p->Nk;
+  a.dq_acc = dq_acc;
+  a.dk = dk;
+  a.dv = dv;
+  a.trace = g_trace;
+  auto kern = sigattn_bwd128_kernel<kBf16>;
+  if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
+  const int grid = std::max(1, std::min(num_sms(), max_items));
+  prof_record(2, s);
+  kern<<<grid, Bwd128Cfg::kThreads, Bwd128Cfg::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
   prof_record(3, s);
   count_launch();
   CUDA_TRY(cudaGetLastError());
@@ -349,7 +389,6 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   const size_t need = sigattn_bwd_workspace_bytes(p);
   if (workspace_bytes < need)
     return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
-  if (p->d != 64) return fail(SIGATTN_EUNSUPPORTED, "backward: d = 128 not implemented in this build");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool dq_f32 = (p->flags & SIGATTN_F_DQ_F32_PARTIAL) != 0;
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
@@ -369,8 +408,12 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   if ((st = launch_zero_rows(dk, row16, p, p->Nk, p->seqlens_k, p->seqlens_q, p->Nq, 0, s)) != SIGATTN_OK) return st;
   if ((st = launch_zero_rows(dv, row16, p, p->Nk, p->seqlens_k, p->seqlens_q, p->Nq, 0, s)) != SIGATTN_OK) return st;
   const bool bf = p->dtype == SIGATTN_BF16;
-  st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s)
-          : launch_bwd<64, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s);
+  if (p->d == 64)
+    st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s)
+            : launch_bwd<64, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s);
+  else
+    st = bf ? launch_bwd128<true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s)
+            : launch_bwd128<false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s);
   if (st != SIGATTN_OK) return st;
   if (!dq_f32) {
     const long long total8 = (long long)p->B * p->H * p->Nq * p->d / 8;

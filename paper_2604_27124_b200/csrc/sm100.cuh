@@ -16,6 +16,13 @@
 
 namespace sm100 {
 
+__device__ __forceinline__ void trace_globaltime(long long* buf, int slot) {
+#if SIGATTN_TRACE
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (buf) buf[(size_t)blockIdx.x * 4096 + slot] = t;
+#endif
+}
 __device__ __forceinline__ void trace_event(long long* buf, int slot, int limit) {
 #if SIGATTN_TRACE
   if (buf && slot < limit) buf[(size_t)blockIdx.x * 4096 + slot] = clock64();

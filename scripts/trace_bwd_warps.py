@@ -22,14 +22,14 @@ sa.sigattn_bwd(q, k, v, do, nq, nk, 1 / 8, -math.log(8192))
 torch.cuda.synchronize()
 lib.sigattn_set_trace_buffer(None)
 t = buf.view(148, 4096).cpu().numpy()
-names = ["c0 ld+sigma", "waits", "c0 stores", "c1 ld+sigma+STTM", "c1 STS", "-", "wait_st+fences+arrive"]
 for cta in (0, 77):
     r = t[cta]
-    ev = r[4 * 512:6 * 512].reshape(16, 8, 8)   # warp, tile, event
-    print(f"CTA {cta}: median over tiles 2..7 of phase durations per warp: " + " | ".join(names))
+    ev = r[4 * 512:6 * 512].reshape(16, 8, 8).astype(np.float64)   # warp, tile (8..15), event
+    t0 = ev[0, 0, 0]
+    print(f"CTA {cta}: per warp median over 8 tiles: h0[ld+compute, STTM+STS+wait_st, fences+arrive] |"
+          f" h1 [s_full wait+ld+compute, STTM, STS+wait_st, fences+arrive]")
     for w in range(16):
-        e2 = ev[w, 2:8, :].copy()
-        e2[:, 5] = e2[:, 6]   # event 5 (c1 sigma) now precedes event 4 in time; reorder 3,5,4,6
-        order = [0, 1, 2, 3, 4, 6, 7]
-        d = np.diff(ev[w, 2:8][:, order], axis=1)
-        print(f"  warp {w:2d}: " + " ".join("%6d" % np.median(d[:, e]) for e in range(6)))
+        e = ev[w]
+        m = lambda a, b: np.median(e[:, b] - e[:, a])  # noqa: E731
+        print(f"  warp {w:2d}: h0 {m(0,1):5.0f} {m(1,2):5.0f} {m(2,3):5.0f} | h1 {m(3,4):5.0f} {m(4,5):5.0f} {m(5,6):5.0f} "
+              f"{m(6,7):5.0f} | next h0 wait {np.median(e[1:, 0] - e[:-1, 7]):5.0f}")

@@ -103,13 +103,21 @@ def test_per_sequence_bias():
     I.Config("d128", B=2, H=2, N=256, d=128, lengths=[256, 97], seed=10),
     I.Config("d128_ragged", B=3, H=2, N=300, d=128, lengths=[300, 129, 1], seed=11),
 ])
-def test_d128_forward(cfg):
-    run_case(cfg, check_bwd=False)
+def test_d128_fwd_bwd(cfg):
+    run_case(cfg)
 
 
-def test_d128_fp16_forward():
+def test_d128_fp16():
     cfg = I.Config("d128f16", B=2, H=2, N=256, d=128, lengths=[256, 97], dtype="fp16", seed=12)
-    run_case(cfg, check_bwd=False, tol=FP16_FWD_TOL)
+    run_case(cfg, tol=FP16_FWD_TOL)
+
+
+@pytest.mark.parametrize("cfg", [
+    I.Config("d128_many", B=9, H=3, N=200, d=128, lengths=[200, 1, 63, 64, 65, 127, 128, 129, 0], seed=18),
+    I.Config("d128_cross", B=2, H=2, N=320, d=128, lengths=[320, 100], Nk=192, lengths_k=[192, 70], seed=19),
+])
+def test_d128_ragged_edges(cfg):
+    run_case(cfg)
 
 
 def test_pad_independence_bitwise():
