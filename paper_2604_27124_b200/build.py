@@ -51,6 +51,14 @@ def build_trace() -> str:
     return out
 
 
+def build_variant(name: str, defines) -> str:
+    """Experimental build with extra -D flags -> libsigattn_<name>.so (selected with $SIGATTN_LIB)."""
+    out = os.path.join(PKG, f"libsigattn_{name}.so")
+    cmd = [NVCC] + NVCC_FLAGS + [f"-D{d}" for d in defines] + [os.path.join(CSRC, "sigattn.cu"), "-o", out]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

@@ -35,6 +35,10 @@
 #include "fwd.cuh"
 #include "sigmoid.cuh"
 
+#ifndef SIGATTN_BWD_SCORES_SS
+#define SIGATTN_BWD_SCORES_SS 0   // 1: S^T / dP^T MMAs read K / V from shared memory instead of TMEM
+#endif
+
 namespace sigattn {
 
 struct BwdArgs {
@@ -239,8 +243,20 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
     };
     // S^T_q = K Q_q^T and dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; A from TMEM)
-    auto mma1 = [&](uint32_t st, uint32_t q) {
+    auto mma1 = [&](uint32_t kvb, uint32_t st, uint32_t q) {
       const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+#if SIGATTN_BWD_SCORES_SS
+      const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+        sm100::mma_ss(tmem + C::kColS + q * 64, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024),
+                      sm100::make_sdesc_sw128(qa + kk * 32, 16, 1024), idesc_s, kk > 0);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+        sm100::mma_ss(tmem + C::kColDP + q * 64, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024),
+                      sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_s, kk > 0);
+#else
+      (void)kvb;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
         sm100::mma_ts(tmem + C::kColS + q * 64, tmem + C::kColK + kk * 8,
@@ -249,6 +265,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       for (int kk = 0; kk < D / 16; ++kk)
         sm100::mma_ts(tmem + C::kColDP + q * 64, tmem + C::kColV + kk * 8,
                       sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_s, kk > 0);
+#endif
       sm100::mma_commit(&s_full[q]);
     };
     // dV += P^T_q dO_q ; dK += dS^T_q Q_q   (M = keys, N = d, K = 64 queries; A from TMEM)
@@ -279,8 +296,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::tc_fence_after();
       if (sm100::elect_one()) {
         copy_kv(cur.item_c & 1);
-        mma1(0, 0);
-        mma1(0, 1);
+        mma1(cur.item_c & 1, 0, 0);
+        mma1(cur.item_c & 1, 0, 1);
       }
       __syncwarp();
     }
@@ -305,7 +322,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           // the copy executes after every earlier MMA (tcgen05 ops of one thread run in order), so
           // S/dP(i, q1) has finished reading the previous K/V columns
           if (nxt.i == 0) copy_kv(nxt.item_c & 1);
-          mma1(st1, 0);
+          mma1(nxt.item_c & 1, st1, 0);
         }
         __syncwarp();
       }
@@ -317,7 +334,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         mma2(st, 1, false);
         sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
         if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
-        if (nxt.valid) mma1(st1, 1);
+        if (nxt.valid) mma1(nxt.item_c & 1, st1, 1);
       }
       __syncwarp();
       sm100::mbar_wait(dq_empty, (t & 1) ^ 1);                   // epilogue drained dQ(t-1)

@@ -3,10 +3,12 @@
 //   O[z, M, h, :] = sum over key tiles N < n_k[z] of  sigma(alpha Q_M K_N^T + b_z) masked  . V_N
 //
 // One CTA per SM (persistent), warp-specialised:
-//   warps 0-15  four sigmoid warpgroups: WG g owns key columns [32g, 32g+32) of every S tile:
-//               tcgen05.ld S -> x = alpha s + b -> sigma -> key mask -> bf16 -> tcgen05.st P
-//               (P aliased onto the first half of its own S columns), then the epilogue for
-//               its quarter of the O columns (padded query rows written as exact 0).
+//   warps 0-15  four sigmoid warpgroups in two pairs that take alternate key tiles (ping-pong: one
+//               pair computes while the other synchronises); within a pair warpgroup g owns key
+//               columns [64g, 64g+64): tcgen05.ld S -> x = alpha s + b -> sigma -> key mask -> bf16
+//               -> tcgen05.st P (aliased onto the first half of its own S columns).  All four
+//               warpgroups then run the epilogue, a quarter of the O columns each (padded query
+//               rows written as exact 0).
 //   warp 16     TMA producer: Q tile (double-buffered) and a K/V ring of kStages tiles
 //   warp 17     MMA issuer (one elected thread): S = Q K^T (SS, both K-major) -> TMEM S[3] ring
 //                                                O += P V  (TS, P from TMEM, V MN-major) -> TMEM O
@@ -108,7 +110,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
     for (int i = 0; i < (int)C::kSBuf; ++i) {
       sm100::mbar_init(&s_full[i], 1);
-      sm100::mbar_init(&p_full[i], 4 * C::kNumWG);   // one arrival per sigmoid warp
+      sm100::mbar_init(&p_full[i], 2 * C::kNumWG);   // the 8 warps of the pair that owns the tile
     }
     for (int i = 0; i < C::kStages; ++i) {
       sm100::mbar_init(&k_full[i], 1);
@@ -235,8 +237,8 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::trace_event(args.trace, 1024 + si, 1536);
 #pragma unroll
           for (int kk = 0; kk < kTile / 16; ++kk) {
-            // P for keys [16kk, 16kk+16): WG g = kk/2 stored its 32 keys packed at S cols [32g, 32g+16)
-            const uint32_t a_col = p_col + (kk >> 1) * 32 + (kk & 1) * 8;
+            // P for keys [16kk, 16kk+16): pair warpgroup kk/4 packed its 64 keys at S cols [64 (kk/4), +32)
+            const uint32_t a_col = p_col + (kk >> 2) * 64 + (kk & 3) * 8;
             sm100::mma_ts(tmem + C::kColO, tmem + a_col,
                           sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
                           (j > 0 || kk > 0) ? 1u : 0u);
@@ -257,7 +259,9 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
   } else if (warp < C::kWarpTMA) {
     // ===================== sigmoid warpgroups + epilogue =====================
-    const uint32_t g = warp >> 2;                // warpgroup: key columns [32g, 32g+32)
+    const uint32_t g = warp >> 2;                // warpgroup (epilogue: O columns [g D/4, (g+1) D/4))
+    const uint32_t pair = warp >> 3;             // warpgroup pair: takes the key tiles with si % 2 == pair
+    const uint32_t gp = g & 1;                   // within the pair: key columns [64 gp, 64 gp + 64)
     const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t row = quarter * 32 + lane;    // tile row = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
@@ -274,23 +278,28 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const bool row_valid = qt * kTile + (int)row < nq;
       for (int j = 0; j < nkt; ++j) {
         const uint32_t si = s_it + j;
-        const uint32_t col = (si % C::kSBuf) * 128 + g * 32;
+        if ((si & 1) != pair) continue;          // the other warpgroup pair takes this key tile
         sm100::mbar_wait(&s_full[si % C::kSBuf], (si / C::kSBuf) & 1);
         if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 2048 + si, 2560);
         sm100::tc_fence_after();
-        const int nvalid = nk - (j * kTile + (int)g * 32);   // valid keys in this warpgroup's 32 columns
-        float r[32];
-        uint32_t pk[16];
-        sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
-        if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
-        else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
-        sm100::tmem_st16(tmem + lane_addr + col, pk);
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const uint32_t col = (si % C::kSBuf) * 128 + gp * 64 + ch * 32;
+          const int nvalid = nk - (j * kTile + (int)gp * 64 + ch * 32);   // valid keys in these 32 columns
+          float r[32];
+          uint32_t pk[16];
+          sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+          if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+          else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+          // P over the first half of this warpgroup's 64 columns (chunk 0's columns are already read)
+          sm100::tmem_st16(tmem + lane_addr + (si % C::kSBuf) * 128 + gp * 64 + ch * 16, pk);
+        }
         sm100::tmem_wait_st();
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&p_full[si % C::kSBuf]);
         if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 2560 + si, 3072);
-        if (lane == 0 && warp == 4 * C::kNumWG - 1) sm100::trace_event(args.trace, 3072 + si, 3584);
+        if (lane == 0 && warp == 8) sm100::trace_event(args.trace, 3072 + si, 3584);
       }
       s_it += nkt;
       // ---- epilogue: O rows of this q tile, columns [g*D/4, g*D/4 + D/4)
