@@ -35,6 +35,9 @@
 #include "fwd.cuh"
 #include "sigmoid.cuh"
 
+#ifndef SIGATTN_BWD_LATE_S
+#define SIGATTN_BWD_LATE_S 0      // 1: issue both halves' next-tile score MMAs after dV/dK of half 1
+#endif
 #ifndef SIGATTN_BWD_SCORES_SS
 #define SIGATTN_BWD_SCORES_SS 0   // 1: S^T / dP^T MMAs read K / V from shared memory instead of TMEM
 #endif
@@ -72,7 +75,7 @@ struct BwdCfg {
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kNumWG = 4;                           // compute warpgroups
   static constexpr int kWarpEpi = 4 * kNumWG, kWarpTMA = kWarpEpi + 4, kWarpMMA = kWarpTMA + 1,
-                       kWarpAlloc = kWarpTMA + 2;
+                       kWarpAlloc = kWarpTMA + 2, kWarpFill = kWarpTMA + 3;
   static constexpr int kThreads = 32 * (kWarpEpi + 8);
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 320, kColDQ = 384, kColK = 448,
@@ -314,7 +317,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::tc_fence_after();
       if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
       __syncwarp();
-      if (nxt.valid) {
+      if (!SIGATTN_BWD_LATE_S && nxt.valid) {
         if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
         sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
         sm100::tc_fence_after();
@@ -334,6 +337,20 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         mma2(st, 1, false);
         sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
         if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
+#if SIGATTN_BWD_LATE_S
+      }
+      __syncwarp();
+      if (nxt.valid) {
+        if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
+        sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
+        sm100::tc_fence_after();
+      }
+      if (sm100::elect_one()) {
+        if (nxt.valid) {
+          if (nxt.i == 0) copy_kv(nxt.item_c & 1);
+          mma1(nxt.item_c & 1, st1, 0);
+        }
+#endif
         if (nxt.valid) mma1(nxt.item_c & 1, st1, 1);
       }
       __syncwarp();
@@ -501,6 +518,11 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       ++item_c;
     }
+  }
+
+  if (warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
+    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
+    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
   }
 
   sm100::tc_fence_before();

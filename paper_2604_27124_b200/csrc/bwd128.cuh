@@ -36,7 +36,7 @@ struct Bwd128Cfg {
   static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
   static constexpr int kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
-  static constexpr int kWarpEpi = 16, kWarpTMA = 20, kWarpMMA = 21, kWarpAlloc = 22;
+  static constexpr int kWarpEpi = 16, kWarpTMA = 20, kWarpMMA = 21, kWarpAlloc = 22, kWarpFill = 23;
   static constexpr int kThreads = 768;
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kColS = 0, kColDP = 64, kColDV = 128, kColDK = 256, kColDQ = 384;
@@ -351,6 +351,11 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       }
       ++item_c;
     }
+  }
+
+  if (warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
+    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
+    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
   }
 
   sm100::tc_fence_before();

@@ -17,6 +17,7 @@
 // by sched.cuh from the device seqlens, so fully padded query tiles are never visited
 // and the key loop stops at ceil(n_k / 128) tiles.
 #pragma once
+#include "sched.cuh"
 #include "sigmoid.cuh"
 #include "sm100.cuh"
 
@@ -35,6 +36,7 @@ struct FwdArgs {
   float scale;
   int B, H, Nq, Nk;
   void* o;                // bf16/fp16 [B,H,Nq,D] or fp32 partial
+  int fill_pad;           // zero the O rows no tile epilogue writes (pad_fill_warp)
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots
 };
 
@@ -52,7 +54,8 @@ struct FwdCfg {
   static constexpr int kNumWG = 4;                          // sigmoid warpgroups: warps [0, 4 kNumWG)
   // Single-thread roles sit in the HIGHEST warp ids: the warp scheduler favours high warp ids, so
   // the MMA / TMA issuers are never starved by the sigmoid warps sharing their sub-partition.
-  static constexpr int kWarpTMA = 4 * kNumWG, kWarpMMA = kWarpTMA + 1, kWarpAlloc = kWarpTMA + 2;
+  static constexpr int kWarpTMA = 4 * kNumWG, kWarpMMA = kWarpTMA + 1, kWarpAlloc = kWarpTMA + 2,
+                       kWarpFill = kWarpTMA + 3;
   static constexpr int kThreads = 32 * (4 * kNumWG + 4);
   static constexpr uint32_t kTmemCols = 512;
   // TMEM columns
@@ -345,6 +348,10 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       ++c;
     }
   }
+
+  if (warp == C::kWarpFill && args.fill_pad)   // padded O rows beyond the last valid tile
+    pad_fill_warp(args.o, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
+                  128, lane);
 
   sm100::tc_fence_before();
   __syncthreads();

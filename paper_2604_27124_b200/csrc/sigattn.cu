@@ -111,14 +111,13 @@ sigattn_status set_smem(K kernel, int bytes) {
   return SIGATTN_OK;
 }
 
+int sched_smem(const sigattn_params* p) { return (4 * p->B + 1) * (int)sizeof(int); }
+
 sigattn_status launch_worklist(int kind, const sigattn_params* p, int4* items, int* n_items, cudaStream_t s) {
-  const int smem = 4 * p->B * (int)sizeof(int);
+  const int smem = sched_smem(p);
   if (smem > 48 * 1024) {
-    static bool set = false;
-    if (!set) {
-      CUDA_TRY(cudaFuncSetAttribute(build_worklist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-      set = true;
-    }
+    sigattn_status st = set_smem(build_worklist_kernel, (4 * kMaxSchedB + 1) * (int)sizeof(int));
+    if (st != SIGATTN_OK) return st;
   }
   build_worklist_kernel<<<1, kSchedThreads, smem, s>>>(kind, p->B, p->H, p->Nq, p->Nk, p->seqlens_q, p->seqlens_k,
                                                         items, n_items);
@@ -127,10 +126,15 @@ sigattn_status launch_worklist(int kind, const sigattn_params* p, int4* items, i
   return SIGATTN_OK;
 }
 
-sigattn_status launch_zero_rows(void* out, int row_bytes, const sigattn_params* p, int N, const int32_t* lens,
-                                const int32_t* gate, int gate_N, int mode, cudaStream_t s) {
-  dim3 grid(std::max(1, std::min(64, cdiv((long long)N * row_bytes / 16, 256))), p->B * p->H);
-  zero_rows_kernel<<<grid, 256, 0, s>>>(out, row_bytes, p->B, p->H, N, lens, gate, gate_N, mode);
+sigattn_status launch_bwd_prep(const sigattn_params* p, int4* items, int* n_items, float* dq_acc, cudaStream_t s) {
+  const int smem = sched_smem(p);
+  if (smem > 48 * 1024) {
+    sigattn_status st = set_smem(bwd_prep_kernel, (4 * kMaxSchedB + 1) * (int)sizeof(int));
+    if (st != SIGATTN_OK) return st;
+  }
+  const int zero_ctas = dq_acc ? num_sms() : 0;
+  bwd_prep_kernel<<<1 + zero_ctas, kSchedThreads, smem, s>>>(p->B, p->H, p->Nq, p->Nk, p->d, p->seqlens_q,
+                                                              p->seqlens_k, items, n_items, dq_acc);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
@@ -159,6 +163,7 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   a.Nq = p->Nq;
   a.Nk = p->Nk;
   a.o = o;
+  a.fill_pad = (p->flags & SIGATTN_F_NO_ZERO_PAD_OUT) ? 0 : 1;
   a.trace = g_trace;
   using C = FwdCfg<D>;
   auto kern = sigattn_fwd_kernel<D, kBf16, kF32>;
@@ -174,8 +179,8 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
 
 template <int D, bool kBf16>
 sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
-                          float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
-                          cudaStream_t s) {
+                          float* dq_acc, void* dk, void* dv,
+                          const int4* items, const int* n_items, int max_items, cudaStream_t s) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
   const int bh = p->B * p->H;
@@ -214,8 +219,8 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
 
 template <bool kBf16>
 sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
-                             float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
-                             cudaStream_t s) {
+                             float* dq_acc, void* dk, void* dv,
+                             const int4* items, const int* n_items, int max_items, cudaStream_t s) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
   const int bh = p->B * p->H;
@@ -274,6 +279,11 @@ sigattn_status get_scratch(cudaStream_t s, size_t bytes, void** out) {
   }
   *out = e.first;
   return SIGATTN_OK;
+}
+
+size_t ws_acc_bytes(const sigattn_params* p) { return align_up((size_t)p->B * p->H * p->Nq * p->d * sizeof(float), 256); }
+size_t ws_items_bytes(const sigattn_params* p) {
+  return align_up(16 + (size_t)p->B * p->H * cdiv(p->Nk, 128) * sizeof(int4), 256);
 }
 
 }  // namespace
@@ -344,7 +354,6 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
     return fail(SIGATTN_EINVAL, "tensor pointers must be 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool f32 = (p->flags & SIGATTN_F_OUT_F32_PARTIAL) != 0;
-  const int elem_out = f32 ? 4 : 2;
   const int max_items = p->B * p->H * cdiv(p->Nq, 128);
   void* scratch = nullptr;
   const size_t bytes = 16 + (size_t)max_items * sizeof(int4);
@@ -352,8 +361,6 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
   int* n_items = reinterpret_cast<int*>(scratch);
   int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(scratch) + 16);
   st = launch_worklist(0, p, items, n_items, s);
-  if (st == SIGATTN_OK && !(p->flags & SIGATTN_F_NO_ZERO_PAD_OUT))
-    st = launch_zero_rows(o, p->d * elem_out, p, p->Nq, p->seqlens_q, p->seqlens_k, p->Nk, 0, s);
   if (st == SIGATTN_OK) {
     const bool bf = p->dtype == SIGATTN_BF16;
     if (p->d == 64) {
@@ -371,11 +378,11 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
   return st;
 }
 
+// Workspace: fp32 dQ accumulator | work list (256-B aligned parts).
+
 size_t sigattn_bwd_workspace_bytes(const sigattn_params* p) {
   if (check_params(p) != SIGATTN_OK) return 0;
-  const size_t acc = (size_t)p->B * p->H * p->Nq * p->d * sizeof(float);
-  const size_t items = 16 + (size_t)p->B * p->H * cdiv(p->Nk, 128) * sizeof(int4);
-  return align_up(acc, 256) + align_up(items, 256);
+  return ws_acc_bytes(p) + ws_items_bytes(p);
 }
 
 sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
@@ -392,41 +399,36 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool dq_f32 = (p->flags & SIGATTN_F_DQ_F32_PARTIAL) != 0;
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-  const size_t acc_bytes = align_up((size_t)p->B * p->H * p->Nq * p->d * sizeof(float), 256);
+  const size_t acc_bytes = ws_acc_bytes(p);
   float* dq_acc = dq_f32 ? reinterpret_cast<float*>(dq) : reinterpret_cast<float*>(ws);
   int* n_items = reinterpret_cast<int*>(ws + acc_bytes);
   int4* items = reinterpret_cast<int4*>(ws + acc_bytes + 16);
   const int max_items = p->B * p->H * cdiv(p->Nk, 128);
-  const int row16 = p->d * 2;
-  if ((st = launch_worklist(1, p, items, n_items, s)) != SIGATTN_OK) return st;
-  // dQ accumulator: valid rows zeroed (padded rows are never touched unless dq is the fp32 output)
-  if (dq_f32) {
-    CUDA_TRY(cudaMemsetAsync(dq, 0, (size_t)p->B * p->H * p->Nq * p->d * sizeof(float), s));
-  } else if ((st = launch_zero_rows(dq_acc, p->d * 4, p, p->Nq, p->seqlens_q, nullptr, -1, 1, s)) != SIGATTN_OK) {
+  // fp32 dQ output (context-parallel partials): plain zero-init, the kernel accumulates into it
+  if (dq_f32) CUDA_TRY(cudaMemsetAsync(dq, 0, (size_t)p->B * p->H * p->Nq * p->d * sizeof(float), s));
+  if ((st = launch_bwd_prep(p, items, n_items, dq_f32 ? nullptr : dq_acc, s)) != SIGATTN_OK)
     return st;
-  }
-  if ((st = launch_zero_rows(dk, row16, p, p->Nk, p->seqlens_k, p->seqlens_q, p->Nq, 0, s)) != SIGATTN_OK) return st;
-  if ((st = launch_zero_rows(dv, row16, p, p->Nk, p->seqlens_k, p->seqlens_q, p->Nq, 0, s)) != SIGATTN_OK) return st;
   const bool bf = p->dtype == SIGATTN_BF16;
   if (p->d == 64)
-    st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s)
-            : launch_bwd<64, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s);
+    st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
+                                   max_items, s)
+            : launch_bwd<64, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
+                                    max_items, s);
   else
-    st = bf ? launch_bwd128<true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s)
-            : launch_bwd128<false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s);
-  if (st != SIGATTN_OK) return st;
-  if (!dq_f32) {
-    const long long total8 = (long long)p->B * p->H * p->Nq * p->d / 8;
-    const int grid = (int)std::min<long long>(4LL * num_sms(), (total8 + 255) / 256);
-    if (bf)
-      dq_finalize_kernel<true><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
-                                                    p->seqlens_q, total8);
-    else
-      dq_finalize_kernel<false><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
-                                                     p->seqlens_q, total8);
-    count_launch();
-    CUDA_TRY(cudaGetLastError());
-  }
+    st = bf ? launch_bwd128<true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
+                                  max_items, s)
+            : launch_bwd128<false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
+                                   max_items, s);
+  if (st != SIGATTN_OK || dq_f32) return st;
+  const dim3 grid(std::max(1, std::min(32, cdiv(p->Nq, 256))), p->B * p->H);
+  if (bf)
+    dq_finalize_kernel<true><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
+                                                  p->seqlens_q);
+  else
+    dq_finalize_kernel<false><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
+                                                   p->seqlens_q);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
 }
 

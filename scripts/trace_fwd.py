@@ -45,13 +45,3 @@ for cta in (0, 77):
               "last parr->MMA pfull %.0f | pfull->PV issued %.0f" % (d(1, 2), d(2, 3), d(3, 4), d(4, 5), d(5, 6)))
         per_tile = np.median(np.diff(a[:, 2]))
         print("median period between consecutive WG s_full: %.0f clk" % per_tile)
-# per-warp phases (si 16..19)
-for cta in (0, 77):
-    r = t[cta]
-    ev = r[3584:3584 + 16 * 4 * 8].reshape(16, 4, 8).astype(np.float64)
-    print(f"CTA {cta} per-warp medians: s_full wait | fence+misc | ld | sigma | st+wait_st | fence+syncwarp | arrive | loop->next wait")
-    for w in range(16):
-        e = ev[w]
-        m = lambda a, b: np.median(e[:, b] - e[:, a])  # noqa: E731
-        nxt = np.median(e[1:, 6] - e[:-1, 5])
-        print(f"  warp {w:2d}: {m(6,7):6.0f} {m(7,0):6.0f} {m(0,1):6.0f} {m(1,2):6.0f} {m(2,3):6.0f} {m(3,4):6.0f} {m(4,5):6.0f} {nxt:6.0f}")

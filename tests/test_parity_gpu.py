@@ -34,12 +34,15 @@ def relerr(got, ref):
     return float(np.abs(got - ref).max() / den)
 
 
-def run_case(cfg, bias=None, check_bwd=True, pad=None, tol=BF16_TOL):
+def run_case(cfg, bias=None, check_bwd=True, pad=None, tol=BF16_TOL, nan_prefill=False):
+    """nan_prefill: outputs are preallocated full of NaN, so every element (padded rows included)
+    must be written by the kernels (the pad fill runs inside the attention kernels)."""
     sa = _sa()
     q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda", pad=pad)
     alpha = 1.0 / math.sqrt(cfg.d)
     b = -math.log(cfg.N_k) if bias is None else bias
-    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b)
+    nan = (lambda t: torch.full_like(t, float("nan"))) if nan_prefill else (lambda t: None)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b, out=nan(q))
     torch.cuda.synchronize()
     bias_np = np.full(cfg.B, b) if np.isscalar(b) else b.double().cpu().numpy()
     ro = oracle.fwd(f64(q), f64(k), f64(v), cfg.nq, cfg.nk, alpha, bias_np)
@@ -49,7 +52,7 @@ def run_case(cfg, bias=None, check_bwd=True, pad=None, tol=BF16_TOL):
         assert torch.all(o[bb, :, cfg.nq[bb]:] == 0), "padded query rows must be exactly 0"
     res = {"o": e}
     if check_bwd:
-        dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b)
+        dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b, dq=nan(q), dk=nan(k), dv=nan(v))
         torch.cuda.synchronize()
         rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, alpha, bias_np)
         for name, got, ref in (("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
@@ -86,6 +89,17 @@ def test_c1_fp16_bwd():
 ])
 def test_ragged_and_edge_cases(cfg):
     run_case(cfg)
+
+
+@pytest.mark.parametrize("cfg", [
+    I.Config("nan_ragged", B=5, H=2, N=300, d=64, lengths=[300, 1, 129, 0, 256], seed=20),
+    I.Config("nan_cross", B=3, H=2, N=320, d=64, lengths=[320, 0, 7], Nk=200, lengths_k=[200, 150, 0], seed=21),
+    I.Config("nan_d128", B=4, H=2, N=300, d=128, lengths=[300, 65, 0, 128], seed=22),
+    I.Config("nan_d128_cross", B=3, H=2, N=200, d=128, lengths=[200, 63, 9], Nk=330, lengths_k=[0, 330, 129], seed=23),
+])
+def test_every_output_element_written(cfg):
+    """Outputs prefilled with NaN: valid rows match the oracle and every padded row is exactly 0."""
+    run_case(cfg, nan_prefill=True)
 
 
 def test_cross_lengths_nq_ne_nk():
