@@ -35,8 +35,20 @@
 #include "fwd.cuh"
 #include "sigmoid.cuh"
 
-#ifndef SIGATTN_BWD_LATE_S
-#define SIGATTN_BWD_LATE_S 0      // 1: issue both halves' next-tile score MMAs after dV/dK of half 1
+#ifndef SIGATTN_BWD_DQ_LATE
+#define SIGATTN_BWD_DQ_LATE 0
+#endif
+#ifndef SIGATTN_DBG_NOCOMPUTE
+#define SIGATTN_DBG_NOCOMPUTE 0   // timing experiments only (wrong results): compute warps skip sigma + TMEM I/O
+#endif
+#ifndef SIGATTN_DBG_EPI_NOLD
+#define SIGATTN_DBG_EPI_NOLD 0    // timing experiments only: epilogue skips TMEM loads and global writes
+#endif
+#ifndef SIGATTN_DBG_NOSTAGE
+#define SIGATTN_DBG_NOSTAGE 0     // timing experiments only (wrong results): epilogue skips the dS smem staging
+#endif
+#ifndef SIGATTN_DBG_MMAONLY
+#define SIGATTN_DBG_MMAONLY 0     // timing experiments only: MMA + TMA pipeline alone (no compute/epilogue waits)
 #endif
 #ifndef SIGATTN_BWD_SCORES_SS
 #define SIGATTN_BWD_SCORES_SS 0   // 1: S^T / dP^T MMAs read K / V from shared memory instead of TMEM
@@ -71,7 +83,7 @@ struct BwdCfg {
   static constexpr int kDSOff = kDOOff + kQStages * kTileBytes;     // dS^T[2]: 2 halves of [128 keys][64 q]
   static constexpr int kDSBytes = 2 * kTile * 128;
   static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
-  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1;
+  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1 + 2 + 2;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kNumWG = 4;                           // compute warpgroups
   static constexpr int kWarpEpi = 4 * kNumWG, kWarpTMA = kWarpEpi + 4, kWarpMMA = kWarpTMA + 1,
@@ -157,6 +169,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* dq_empty = dq_full + 1;
   uint64_t* acc_full = dq_empty + 1;
   uint64_t* acc_empty = acc_full + 1;
+  uint64_t* ds_copied = acc_empty + 1;            // [2] per query half: epilogue read dS^T from TMEM
+  uint64_t* ds_full = ds_copied + 2;              // [2] per dS smem buffer: both halves staged + fenced
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -170,6 +184,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&ds_free[i], 1);
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&p_full[i], kComputeWarps);       // every compute warp works on every half
+      sm100::mbar_init(&ds_copied[i], 4);
+      sm100::mbar_init(&ds_full[i], 8);                  // 4 epilogue warps x 2 halves
     }
     for (int i = 0; i < C::kQStages; ++i) {
       sm100::mbar_init(&qdo_full[i], 1);
@@ -304,22 +320,54 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       __syncwarp();
     }
+    // dQ(t) = dS(t) K after both halves' next-tile score MMAs (SIGATTN_BWD_DQ_LATE=1: one tile
+    // late, between the halves of tile t+1 -- measured slower, 3.03 vs 2.57 ms on C3).
+    uint32_t prev_kvb = 0;
+    bool prev_last = false;      // the tile dQ is pending for was its item's last (frees its K/V slot)
+    auto issue_dq = [&](uint32_t tq) {
+      const uint32_t b2 = tq & 1;
+#if !SIGATTN_DBG_MMAONLY
+      sm100::mbar_wait(dq_empty, (tq & 1) ^ 1);                  // epilogue drained dQ(tq-1)
+      sm100::mbar_wait(&ds_full[b2], (tq >> 1) & 1);             // dS(tq) staged in smem, proxy-fenced
+#endif
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const uint32_t ka = k_base + prev_kvb * C::kTileBytes;
+        const uint32_t dsa = ds_base + b2 * C::kDSBytes;
+        // dQ = dS K   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major, B = K MN-major)
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          sm100::mma_ss(tmem + C::kColDQ, sm100::make_sdesc_sw128(dsa + kk * 2048, kTile * 128, 1024),
+                        sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024), idesc_dq, kk > 0);
+        sm100::mma_commit(&ds_free[b2]);
+        sm100::mma_commit(dq_full);
+        if (prev_last) sm100::mma_commit(&kv_empty[prev_kvb]);   // K/V smem slot free
+      }
+      __syncwarp();
+    };
     uint32_t t = 0;
     while (cur.valid) {
       TileIter nxt = cur;
       nxt.advance(args.items);
-      const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1, buf = t & 1;
+      const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1;
       const uint32_t st1 = (t + 1) % C::kQStages;
       // long wait (a compute phase): poll with back-off so the MMA warp does not steal issue slots
+#if !SIGATTN_DBG_MMAONLY
       sm100::mbar_wait_backoff(&p_full[0], t & 1);
+#endif
       if (lane == 0) sm100::trace_event(args.trace, 0 * 512 + t, 0 * 512 + 512);
+#if !SIGATTN_DBG_MMAONLY
       if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);   // epilogue read previous dV/dK
+#endif
       sm100::tc_fence_after();
       if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
       __syncwarp();
-      if (!SIGATTN_BWD_LATE_S && nxt.valid) {
+      if (nxt.valid) {
         if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
         sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
+#if !SIGATTN_DBG_MMAONLY
+        sm100::mbar_wait(&ds_copied[0], t & 1);      // dS^T(t, q0) left TMEM before S/dP(t+1, q0) land there
+#endif
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
           // the copy executes after every earlier MMA (tcgen05 ops of one thread run in order), so
@@ -329,58 +377,48 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         }
         __syncwarp();
       }
+#if SIGATTN_BWD_DQ_LATE
+      if (t > 0) issue_dq(t - 1);
+#endif
       if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
+#if !SIGATTN_DBG_MMAONLY
       sm100::mbar_wait_backoff(&p_full[1], t & 1);
+#endif
       if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
       sm100::tc_fence_after();
       if (sm100::elect_one()) {
         mma2(st, 1, false);
         sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
         if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
-#if SIGATTN_BWD_LATE_S
       }
       __syncwarp();
       if (nxt.valid) {
-        if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
-        sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
-        sm100::tc_fence_after();
-      }
-      if (sm100::elect_one()) {
-        if (nxt.valid) {
-          if (nxt.i == 0) copy_kv(nxt.item_c & 1);
-          mma1(nxt.item_c & 1, st1, 0);
-        }
+#if !SIGATTN_DBG_MMAONLY
+        sm100::mbar_wait(&ds_copied[1], t & 1);
 #endif
-        if (nxt.valid) mma1(nxt.item_c & 1, st1, 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 1);
+        __syncwarp();
       }
-      __syncwarp();
-      sm100::mbar_wait(dq_empty, (t & 1) ^ 1);                   // epilogue drained dQ(t-1)
-      sm100::tc_fence_after();
-      if (sm100::elect_one()) {
-        const uint32_t ka = k_base + kvb * C::kTileBytes;
-        const uint32_t dsa = ds_base + buf * C::kDSBytes;
-        // dQ = dS K   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major, B = K MN-major)
-#pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk)
-          sm100::mma_ss(tmem + C::kColDQ, sm100::make_sdesc_sw128(dsa + kk * 2048, kTile * 128, 1024),
-                        sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024), idesc_dq, kk > 0);
-        sm100::mma_commit(&ds_free[buf]);
-        sm100::mma_commit(dq_full);
-        if (cur.i == cur.nqt - 1) sm100::mma_commit(&kv_empty[kvb]);   // K/V smem slot free
-      }
-      __syncwarp();
+      prev_kvb = kvb;
+      prev_last = cur.i == cur.nqt - 1;
+#if !SIGATTN_BWD_DQ_LATE
+      issue_dq(t);
+#endif
       if (lane == 0) sm100::trace_event(args.trace, 3 * 512 + t, 3 * 512 + 512);
       cur = nxt;
       ++t;
     }
-  } else if (warp < kComputeWarps) {
+#if SIGATTN_BWD_DQ_LATE
+    if (t > 0) issue_dq(t - 1);
+#endif
+  } else if (warp < kComputeWarps && !SIGATTN_DBG_MMAONLY) {
     // ===================== compute warps: all 16 work on each query half in turn =====================
     // warpgroup w4 owns queries [16 w4, 16 w4 + 16) of each 64-query half
     const uint32_t w4 = warp >> 2;
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
-    const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
     uint32_t t = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
@@ -394,15 +432,20 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       for (int i = 0; i < nqt; ++i, ++t) {
-        const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
 #pragma unroll
         for (int qh = 0; qh < 2; ++qh) {
           sm100::mbar_wait(&s_full[qh], t & 1);
 #define BWD_TR(e) if (lane == 0 && t >= 8 && t < 16) sm100::trace_event(args.trace, 4 * 512 + (warp * 8 + (t - 8)) * 8 + (e), 6 * 512)
-          if (qh == 0) BWD_TR(0);
-          if (qh == 0) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) done with it
+          BWD_TR(qh == 0 ? 0 : 3);
           sm100::tc_fence_after();
           const uint32_t s_col = C::kColS + qh * 64 + w4 * 16, dp_col = C::kColDP + qh * 64 + w4 * 16;
+#if SIGATTN_DBG_NOCOMPUTE
+          if (true) {
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
+            continue;
+          }
+#endif
           float s[16], dp[16];
           sm100::tmem_ld16(tmem + lane_addr + s_col, s);
           sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
@@ -415,35 +458,66 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16);
           else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
           BWD_TR(qh == 0 ? 1 : 4);
-          // P^T / dS^T over the first half of this warp's own (already read) columns
+          // P^T / dS^T over the first half of this warp's own (already read) columns; the epilogue
+          // warpgroup stages dS^T into shared memory for the dQ MMA
           sm100::tmem_st8(tmem + lane_addr + s_col, pp);
           sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
-          if (qh == 1) BWD_TR(5);
-          // dS^T into the swizzled smem tile: half qh, 16 queries = 16-byte chunks 2 w4, 2 w4 + 1
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const uint32_t chunk = (uint32_t)(w4 * 2 + u) ^ (row & 7);
-            sm100::st_shared_v4(dsr + qh * (kTile * 128) + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2],
-                                dd[4 * u + 3]);
-          }
           sm100::tmem_wait_st();
-          BWD_TR(qh == 0 ? 2 : 6);
-          sm100::fence_proxy_async_smem();
           sm100::tc_fence_before();
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&p_full[qh]);
-          BWD_TR(qh == 0 ? 3 : 7);
+          BWD_TR(qh == 0 ? 2 : 5);
 #undef BWD_TR
         }
       }
     }
-  } else if (warp < C::kWarpTMA) {
-    // ===================== epilogue warpgroup: dQ drain + dK/dV =====================
+  } else if (warp < C::kWarpTMA && !SIGATTN_DBG_MMAONLY && warp >= kComputeWarps) {
+    // ===================== epilogue warpgroup: dS^T staging, dQ drain, dK/dV =====================
+    // Per query tile t: for each half, copy the packed dS^T the compute warps left in TMEM into the
+    // swizzled smem operand of the dQ MMA (so the compute warps never wait on shared-memory stores or
+    // proxy fences), then drain dQ(t-1) -- one tile behind, so the drain never delays the copies the
+    // MMA warp is waiting for.
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;
     const uint32_t lane_addr = (quarter * 32) << 16;
+    const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
     const float alpha = args.scale;
+    // dQ(t) rows of this thread += alpha * TMEM dQ  (valid query rows only)
+    auto drain_dq = [&](uint32_t tq, size_t zh, int i, int nq) {
+      sm100::mbar_wait(dq_full, tq & 1);
+      sm100::tc_fence_after();
+      const int q = i * kTile + (int)row;
+      float* dst = args.dq_acc + (zh * args.Nq + q) * D;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {     // two 32-column halves (register budget)
+        float r[2][16];
+        if (SIGATTN_DBG_EPI_NOLD) {
+          if (hh == 1 && lane == 0) sm100::mbar_arrive(dq_empty);
+          continue;
+        }
+        sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + hh * 32, r[0]);
+        sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + hh * 32 + 16, r[1]);
+        sm100::tmem_wait_ld_dep16(r[0]);
+        sm100::tmem_wait_ld_dep16(r[1]);
+        if (hh == 1) {
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(dq_empty);
+        }
+        if (q < nq) {
+#pragma unroll
+          for (int c4 = 0; c4 < 2; ++c4)
+#pragma unroll
+            for (int e = 0; e < 16; e += 4)
+              red_add_v4(dst + hh * 32 + c4 * 16 + e, alpha * r[c4][e], alpha * r[c4][e + 1], alpha * r[c4][e + 2],
+                         alpha * r[c4][e + 3]);
+        }
+      }
+    };
     uint32_t t = 0, item_c = 0;
+    bool pend = false;            // a dQ tile waiting to be drained
+    size_t pend_zh = 0;
+    int pend_i = 0, pend_nq = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
@@ -452,31 +526,33 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const size_t zh = (size_t)(b * args.H + h);
       for (int i = 0; i < nqt; ++i, ++t) {
-        sm100::mbar_wait_backoff(dq_full, t & 1);
-        sm100::tc_fence_after();
-        const int q = i * kTile + (int)row;
-        float* dst = args.dq_acc + (zh * args.Nq + q) * D;
+        const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
+#pragma unroll 1
+        for (int qh = 0; qh < 2; ++qh) {
+          sm100::mbar_wait(&p_full[qh], t & 1);
+          sm100::tc_fence_after();
+          uint32_t d[4][8];   // packed dS^T of queries [64 qh + 16 g, +16) at columns 64 qh + 16 g + [0, 8)
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {     // two 32-column halves (register budget)
-          float r[2][16];
-          sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + hh * 32, r[0]);
-          sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + hh * 32 + 16, r[1]);
-          sm100::tmem_wait_ld_dep16(r[0]);
-          sm100::tmem_wait_ld_dep16(r[1]);
-          if (hh == 1) {
-            sm100::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(dq_empty);
-          }
-          if (q < nq) {
+          for (int g = 0; g < 4 * !SIGATTN_DBG_EPI_NOLD; ++g)
+            sm100::tmem_ld8(tmem + lane_addr + C::kColDP + qh * 64 + g * 16, d[g]);
+          sm100::tmem_wait_ld_dep4x8(d);
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&ds_copied[qh]);
+          if (qh == 0) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) done with the buffer
 #pragma unroll
-            for (int c4 = 0; c4 < 2; ++c4)
-#pragma unroll
-              for (int e = 0; e < 16; e += 4)
-                red_add_v4(dst + hh * 32 + c4 * 16 + e, alpha * r[c4][e], alpha * r[c4][e + 1], alpha * r[c4][e + 2],
-                           alpha * r[c4][e + 3]);
-          }
+          for (int c = 0; c < 8 * !SIGATTN_DBG_NOSTAGE; ++c)   // 16-byte chunk c = queries [8c, 8c + 8) of this half, SW128 swizzle
+            sm100::st_shared_v4(dsr + qh * (kTile * 128) + ((c ^ (row & 7)) * 16), d[c >> 1][(c & 1) * 4],
+                                d[c >> 1][(c & 1) * 4 + 1], d[c >> 1][(c & 1) * 4 + 2], d[c >> 1][(c & 1) * 4 + 3]);
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&ds_full[t & 1]);
         }
+        if (pend) drain_dq(t - 1, pend_zh, pend_i, pend_nq);
+        pend = true;
+        pend_zh = zh;
+        pend_i = i;
+        pend_nq = nq;
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
       sm100::mbar_wait_backoff(acc_full, item_c & 1);
@@ -492,6 +568,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           float r[2][16];
+          if (SIGATTN_DBG_EPI_NOLD) {
+            if (which == 1 && hh == 1 && lane == 0) sm100::mbar_arrive(acc_empty);
+            continue;
+          }
           sm100::tmem_ld16(tmem + lane_addr + col + hh * 32, r[0]);
           sm100::tmem_ld16(tmem + lane_addr + col + hh * 32 + 16, r[1]);
           sm100::tmem_wait_ld_dep16(r[0]);
@@ -518,6 +598,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       ++item_c;
     }
+    if (pend) drain_dq(t - 1, pend_zh, pend_i, pend_nq);
   }
 
   if (warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes

@@ -294,6 +294,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], "
@@ -352,6 +357,18 @@ __device__ __forceinline__ void tmem_wait_ld_dep16(float (&r)[16]) {
                : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]), "+r"(u[7]),
                  "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]), "+r"(u[14]),
                  "+r"(u[15])
+               :
+               : "memory");
+}
+// wait for four outstanding x8 loads; the "+r" operands keep their consumers after the wait
+__device__ __forceinline__ void tmem_wait_ld_dep4x8(uint32_t (&u)[4][8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(u[0][0]), "+r"(u[0][1]), "+r"(u[0][2]), "+r"(u[0][3]), "+r"(u[0][4]), "+r"(u[0][5]),
+                 "+r"(u[0][6]), "+r"(u[0][7]), "+r"(u[1][0]), "+r"(u[1][1]), "+r"(u[1][2]), "+r"(u[1][3]),
+                 "+r"(u[1][4]), "+r"(u[1][5]), "+r"(u[1][6]), "+r"(u[1][7]), "+r"(u[2][0]), "+r"(u[2][1]),
+                 "+r"(u[2][2]), "+r"(u[2][3]), "+r"(u[2][4]), "+r"(u[2][5]), "+r"(u[2][6]), "+r"(u[2][7]),
+                 "+r"(u[3][0]), "+r"(u[3][1]), "+r"(u[3][2]), "+r"(u[3][3]), "+r"(u[3][4]), "+r"(u[3][5]),
+                 "+r"(u[3][6]), "+r"(u[3][7])
                :
                : "memory");
 }
