@@ -44,6 +44,9 @@
 #ifndef SIGATTN_DBG_EPI_NOLD
 #define SIGATTN_DBG_EPI_NOLD 0    // timing experiments only: epilogue skips TMEM loads and global writes
 #endif
+#ifndef SIGATTN_DBG_NORED
+#define SIGATTN_DBG_NORED 0       // timing experiments only: skip the dQ reduce-add into global memory
+#endif
 #ifndef SIGATTN_DBG_NOSTAGE
 #define SIGATTN_DBG_NOSTAGE 0     // timing experiments only (wrong results): epilogue skips the dS smem staging
 #endif
@@ -94,10 +97,6 @@ struct BwdCfg {
                             kColV = 480;
 };
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
 
 // Walks this CTA's non-empty work items (static stride) and their query tiles.
 struct TileIter {
@@ -153,7 +152,7 @@ template <int D, bool kBf16>
 __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
 sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                   const BwdArgs args) {
+                   const __grid_constant__ CUtensorMap tmDQ, const BwdArgs args) {
   using C = BwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -482,14 +481,17 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t lane_addr = (quarter * 32) << 16;
     const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
     const float alpha = args.scale;
-    // dQ(t) rows of this thread += alpha * TMEM dQ  (valid query rows only)
-    auto drain_dq = [&](uint32_t tq, size_t zh, int i, int nq) {
+    // dQ(tq) += alpha * TMEM dQ through the TMA: the fp32 tile is written (SW128, two 32-column
+    // boxes) into the dS buffer dQ(tq) has just finished reading, then one thread issues two bulk
+    // tensor reduce-adds into the fp32 accumulator (the adds happen in L2; no per-lane atomics).
+    constexpr uint32_t kEpiThread0 = 32 * kComputeWarps;
+    auto drain_dq = [&](uint32_t tq, int zh, int i) {
       sm100::mbar_wait(dq_full, tq & 1);
       sm100::tc_fence_after();
-      const int q = i * kTile + (int)row;
-      float* dst = args.dq_acc + (zh * args.Nq + q) * D;
+      uint8_t* buf = smem + C::kDSOff + (tq & 1) * C::kDSBytes;
+      const uint32_t sb = sm100::smem_u32(buf) + row * 128;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {     // two 32-column halves (register budget)
+      for (int hh = 0; hh < 2; ++hh) {     // columns [32 hh, 32 hh + 32) -> box hh
         float r[2][16];
         if (SIGATTN_DBG_EPI_NOLD) {
           if (hh == 1 && lane == 0) sm100::mbar_arrive(dq_empty);
@@ -504,20 +506,26 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(dq_empty);
         }
-        if (q < nq) {
 #pragma unroll
-          for (int c4 = 0; c4 < 2; ++c4)
-#pragma unroll
-            for (int e = 0; e < 16; e += 4)
-              red_add_v4(dst + hh * 32 + c4 * 16 + e, alpha * r[c4][e], alpha * r[c4][e + 1], alpha * r[c4][e + 2],
-                         alpha * r[c4][e + 3]);
-        }
+        for (int c = 0; c < 8; ++c)   // 16-byte chunk c (columns 4c..4c+3) at slot c ^ (row & 7)
+          sm100::st_shared_v4(sb + hh * (kTile * 128) + ((c ^ (row & 7)) * 16),
+                              __float_as_uint(alpha * r[c >> 2][(c & 3) * 4]),
+                              __float_as_uint(alpha * r[c >> 2][(c & 3) * 4 + 1]),
+                              __float_as_uint(alpha * r[c >> 2][(c & 3) * 4 + 2]),
+                              __float_as_uint(alpha * r[c >> 2][(c & 3) * 4 + 3]));
+      }
+      sm100::fence_proxy_async_smem();
+      sm100::named_bar_sync(1, 128);
+      if (threadIdx.x == kEpiThread0 && !SIGATTN_DBG_NORED) {
+        // rows past Nq are clipped by the TMA; padded query rows add exact zeros (dS = 0 there)
+        sm100::tma_reduce_add_3d(&tmDQ, buf, 0, i * kTile, zh);
+        sm100::tma_reduce_add_3d(&tmDQ, buf + kTile * 128, 32, i * kTile, zh);
+        sm100::bulk_commit_group();
       }
     };
     uint32_t t = 0, item_c = 0;
     bool pend = false;            // a dQ tile waiting to be drained
-    size_t pend_zh = 0;
-    int pend_i = 0, pend_nq = 0;
+    int pend_zh = 0, pend_i = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
@@ -539,7 +547,11 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::tc_fence_before();
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&ds_copied[qh]);
-          if (qh == 0) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) done with the buffer
+          if (qh == 0) {
+            sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) MMA done with the buffer
+            if (threadIdx.x == kEpiThread0) sm100::bulk_wait_group_read<0>();   // ... and its reduce-add
+            sm100::named_bar_sync(1, 128);
+          }
 #pragma unroll
           for (int c = 0; c < 8 * !SIGATTN_DBG_NOSTAGE; ++c)   // 16-byte chunk c = queries [8c, 8c + 8) of this half, SW128 swizzle
             sm100::st_shared_v4(dsr + qh * (kTile * 128) + ((c ^ (row & 7)) * 16), d[c >> 1][(c & 1) * 4],
@@ -548,11 +560,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&ds_full[t & 1]);
         }
-        if (pend) drain_dq(t - 1, pend_zh, pend_i, pend_nq);
+        if (pend) drain_dq(t - 1, pend_zh, pend_i);
         pend = true;
-        pend_zh = zh;
+        pend_zh = (int)zh;
         pend_i = i;
-        pend_nq = nq;
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
       sm100::mbar_wait_backoff(acc_full, item_c & 1);
@@ -598,7 +609,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       ++item_c;
     }
-    if (pend) drain_dq(t - 1, pend_zh, pend_i, pend_nq);
+    if (pend) drain_dq(t - 1, pend_zh, pend_i);
+    if (threadIdx.x == kEpiThread0) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
   }
 
   if (warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes

@@ -189,6 +189,8 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
   if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
   if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  CUtensorMap tdq;   // fp32 dQ accumulator, 32-column boxes for the TMA reduce-add
+  if ((st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, bh)) != SIGATTN_OK) return st;
   BwdArgs a;
   a.items = items;
   a.n_items = n_items;
@@ -210,7 +212,7 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);
-  kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
+  kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, tdo, tdq, a);
   prof_record(3, s);
   count_launch();
   CUDA_TRY(cudaGetLastError());
