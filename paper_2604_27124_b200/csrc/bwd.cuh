@@ -50,6 +50,9 @@
 #ifndef SIGATTN_DBG_NOSTAGE
 #define SIGATTN_DBG_NOSTAGE 0     // timing experiments only (wrong results): epilogue skips the dS smem staging
 #endif
+#ifndef SIGATTN_BWD_EMU
+#define SIGATTN_BWD_EMU 0         // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
+#endif
 #ifndef SIGATTN_DBG_MMAONLY
 #define SIGATTN_DBG_MMAONLY 0     // timing experiments only: MMA + TMA pipeline alone (no compute/epilogue waits)
 #endif
@@ -131,7 +134,7 @@ struct TileIter {
 template <bool kMask, bool kBf16>
 __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
                                           float a2, float b2, bool key_valid, int nvalid) {
-  sigma_row<16, kMask>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
+  sigma_row<16, kMask, SIGATTN_BWD_EMU>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
 #pragma unroll
   for (int e = 0; e < 16; e += 2) {
     float p0 = v[e], p1 = v[e + 1], u0, u1, d0, d1;

@@ -21,6 +21,10 @@
 #include "sigmoid.cuh"
 #include "sm100.cuh"
 
+#ifndef SIGATTN_FWD_EMU
+#define SIGATTN_FWD_EMU 0   // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
+#endif
+
 namespace sigattn {
 
 constexpr int kTile = 128;           // B_M = B_N = 128 (UMMA M = 128, one TMEM lane per row)
@@ -71,7 +75,7 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 template <bool kMask, bool kBf16>
 __device__ __forceinline__ void sigmoid_row32(float (&v)[32], uint32_t (&pk)[16], float a, float c, bool row_valid,
                                               int nvalid) {
-  sigma_row<32, kMask>(v, a, c, row_valid, nvalid);
+  sigma_row<32, kMask, SIGATTN_FWD_EMU>(v, a, c, row_valid, nvalid);
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
     float p0 = v[e], p1 = v[e + 1];

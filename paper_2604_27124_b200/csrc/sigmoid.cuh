@@ -82,6 +82,47 @@ __device__ __forceinline__ void sigma2_fast(float t0, float t1, float& p0, float
   fmul2(p0, p1, r0, r1, u0, u1);                    // u R(u)
 }
 
+__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// 2^t on the FMA pipe (no MUFU), for t <= kFastT: t = j + f with j = rint(t) (magic-number
+// rounding) and f in [-1/2, 1/2];  2^f ~ E(f), a degree-3 relative-minimax polynomial (max rel.
+// error 7.5e-5);  the exponent j is added to E's bit pattern with one integer multiply-add.
+// t is clamped at -125 so that the exponent field cannot underflow (sigma < 2^-125 rounds to 0).
+// Used for a fixed subset of the element pairs so that the MUFU and FMA pipes share the exp2 work.
+constexpr float kE0 = 0.9999280735404956f, kE1 = 0.6932609854573364f, kE2 = 0.24261112219433045f,
+                kE3 = 0.05517166907486297f;
+constexpr float kRoundMagic = 12582912.0f;   // 1.5 * 2^23
+__device__ __forceinline__ void exp2_fma2(float t0, float t1, float& u0, float& u1) {
+  t0 = fmaxf(t0, -125.0f);
+  t1 = fmaxf(t1, -125.0f);
+  float y0, y1, j0, j1, f0, f1, e0, e1;
+  fadd2(y0, y1, t0, t1, kRoundMagic, kRoundMagic);          // low mantissa bits of y = rint(t)
+  fadd2(j0, j1, y0, y1, -kRoundMagic, -kRoundMagic);        // rint(t)
+  ffma2(f0, f1, j0, j1, -1.0f, -1.0f, t0, t1);              // f = t - rint(t)
+  ffma2(e0, e1, f0, f1, kE3, kE3, kE2, kE2);
+  ffma2(e0, e1, e0, e1, f0, f1, kE1, kE1);
+  ffma2(e0, e1, e0, e1, f0, f1, kE0, kE0);
+  // bits(2^t) = bits(E) + j << 23;  bits(y) = 0x4B400000 + j and 0x4B400000 << 23 == 0 (mod 2^32)
+  u0 = __uint_as_float(__float_as_uint(y0) * (1u << 23) + __float_as_uint(e0));
+  u1 = __uint_as_float(__float_as_uint(y1) * (1u << 23) + __float_as_uint(e1));
+}
+
+// sigma2_fast with the exp2 on the FMA pipe.
+__device__ __forceinline__ void sigma2_fast_fma(float t0, float t1, float& p0, float& p1) {
+  float u0, u1;
+  exp2_fma2(t0, t1, u0, u1);
+  float r0, r1;
+  ffma2(r0, r1, u0, u1, kR2, kR2, kR1, kR1);
+  ffma2(r0, r1, r0, r1, u0, u1, kR0, kR0);
+  fmul2(p0, p1, r0, r1, u0, u1);
+}
+
 // p = sigma(x) from t = x log2 e, any range (the reciprocal path of sigma2).
 __device__ __forceinline__ void sigma2_from_t(float t0, float t1, float& p0, float& p1) {
   // 1 / (1 + 2^-t), with -t clamped at 126 so that 1 + 2^-t stays finite
@@ -103,7 +144,9 @@ __device__ __forceinline__ void sigma2_from_t(float t0, float t1, float& p0, flo
 // a = alpha log2 e, c = b log2 e (so t = x log2 e = s a + c).  The path vote only looks at valid
 // elements (lane_valid rows, columns < nvalid when kMask): padding can never change which
 // arithmetic the valid outputs see, so results stay bitwise independent of pad content.
-template <int N, bool kMask = false>
+// kEmuEvery > 0: in the fast path, element pairs with index % kEmuEvery == kEmuEvery / 2 take the
+// FMA-pipe exp2 (exp2_fma2) instead of MUFU ex2, off-loading the MUFU unit (16 ops/clk/SM).
+template <int N, bool kMask = false, int kEmuEvery = 0>
 __device__ __forceinline__ void sigma_row(float (&v)[N], float a, float c, bool lane_valid = true, int nvalid = N) {
   float m = -INFINITY;
 #pragma unroll
@@ -116,7 +159,12 @@ __device__ __forceinline__ void sigma_row(float (&v)[N], float a, float c, bool 
   }
   if (__all_sync(0xffffffffu, !lane_valid || m <= kFastT)) {
 #pragma unroll
-    for (int e = 0; e < N; e += 2) sigma2_fast(v[e], v[e + 1], v[e], v[e + 1]);
+    for (int e = 0; e < N; e += 2) {
+      if (kEmuEvery > 0 && (e / 2) % (kEmuEvery > 0 ? kEmuEvery : 1) == kEmuEvery / 2)
+        sigma2_fast_fma(v[e], v[e + 1], v[e], v[e + 1]);
+      else
+        sigma2_fast(v[e], v[e + 1], v[e], v[e + 1]);
+    }
   } else {
 #pragma unroll
     for (int e = 0; e < N; e += 2) sigma2_from_t(v[e], v[e + 1], v[e], v[e + 1]);
