@@ -35,6 +35,17 @@
 #include "fwd.cuh"
 #include "sigmoid.cuh"
 
+#ifndef SIGATTN_BWD_MMA_SPIN
+#define SIGATTN_BWD_MMA_SPIN 0    // 1: the MMA warp spins (no nanosleep back-off) on p_full
+#endif
+#if SIGATTN_BWD_MMA_SPIN
+#define MMA_WAIT_P(b, p) sm100::mbar_wait(b, p)
+#else
+#define MMA_WAIT_P(b, p) sm100::mbar_wait_backoff(b, p)
+#endif
+#ifndef SIGATTN_BWD_DRAIN_EARLY
+#define SIGATTN_BWD_DRAIN_EARLY 0
+#endif
 #ifndef SIGATTN_BWD_DQ_LATE
 #define SIGATTN_BWD_DQ_LATE 0
 #endif
@@ -355,7 +366,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t st1 = (t + 1) % C::kQStages;
       // long wait (a compute phase): poll with back-off so the MMA warp does not steal issue slots
 #if !SIGATTN_DBG_MMAONLY
-      sm100::mbar_wait_backoff(&p_full[0], t & 1);
+      MMA_WAIT_P(&p_full[0], t & 1);
 #endif
       if (lane == 0) sm100::trace_event(args.trace, 0 * 512 + t, 0 * 512 + 512);
 #if !SIGATTN_DBG_MMAONLY
@@ -384,7 +395,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #endif
       if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
 #if !SIGATTN_DBG_MMAONLY
-      sm100::mbar_wait_backoff(&p_full[1], t & 1);
+      MMA_WAIT_P(&p_full[1], t & 1);
 #endif
       if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
       sm100::tc_fence_after();
@@ -562,8 +573,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&ds_full[t & 1]);
+          // SIGATTN_BWD_DRAIN_EARLY: drain dQ(t-1) between the two halves of tile t
+          if (SIGATTN_BWD_DRAIN_EARLY && qh == 0 && pend) drain_dq(t - 1, pend_zh, pend_i);
         }
-        if (pend) drain_dq(t - 1, pend_zh, pend_i);
+        if (!SIGATTN_BWD_DRAIN_EARLY && pend) drain_dq(t - 1, pend_zh, pend_i);
         pend = true;
         pend_zh = (int)zh;
         pend_i = i;
@@ -616,7 +629,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     if (threadIdx.x == kEpiThread0) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
   }
 
-  if (warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
+  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
     pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
     pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
   }

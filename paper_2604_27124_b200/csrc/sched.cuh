@@ -7,6 +7,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef SIGATTN_DBG_NOFILL
+#define SIGATTN_DBG_NOFILL 0   // timing experiments only (outputs incomplete): skip the padded-row fills
+#endif
+
 namespace sigattn {
 
 constexpr int kSchedThreads = 1024;
