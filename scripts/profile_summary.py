@@ -81,9 +81,9 @@ def main(tag):
     fwd = next((v for n, v in kern.items() if "fwd_kernel" in n), {})
     summ = {"tag": tag,
             "bwd_kernel": {"dram_bytes_per_launch": bwd.get("dram__bytes_read.sum", 0) + bwd.get("dram__bytes_write.sum", 0),
-                           "duration_ns": bwd.get("gpu__time_duration.sum")},
+                           "duration_ms": bwd.get("gpu__time_duration.sum")},
             "fwd_kernel": {"dram_bytes_per_launch": fwd.get("dram__bytes_read.sum", 0) + fwd.get("dram__bytes_write.sum", 0),
-                           "duration_ns": fwd.get("gpu__time_duration.sum")}}
+                           "duration_ms": fwd.get("gpu__time_duration.sum")}}
     json.dump(summ, open(os.path.join(out, "ncu_summary.json"), "w"), indent=1)
     print("\n".join(lines))
 
