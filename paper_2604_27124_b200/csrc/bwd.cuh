@@ -92,14 +92,15 @@ template <int D>
 struct BwdCfg {
   static_assert(D == 64, "fused backward: d = 64 TMEM plan");
   static constexpr int kTileBytes = kTile * D * 2;           // 16 KB
-  static constexpr int kQStages = 3;                         // Q_i + dO_i ring
+  static constexpr int kQStages = 2;                         // Q_i + dO_i ring
   static constexpr int kKOff = 0;                            // K[2]
   static constexpr int kVOff = kKOff + 2 * kTileBytes;       // V[2]
   static constexpr int kQOff = kVOff + 2 * kTileBytes;       // Q[kQStages]
   static constexpr int kDOOff = kQOff + kQStages * kTileBytes;      // dO[kQStages]
   static constexpr int kDSOff = kDOOff + kQStages * kTileBytes;     // dS^T[2]: 2 halves of [128 keys][64 q]
   static constexpr int kDSBytes = 2 * kTile * 128;
-  static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
+  static constexpr int kDQOff = kDSOff + 2 * kDSBytes;      // fp32 dQ staging tile for the TMA reduce-add
+  static constexpr int kBarOff = kDQOff + kTile * D * 4;
   static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1 + 2 + 2;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kNumWG = 4;                           // compute warpgroups
@@ -448,7 +449,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
         for (int qh = 0; qh < 2; ++qh) {
           sm100::mbar_wait(&s_full[qh], t & 1);
-#define BWD_TR(e) if (lane == 0 && t >= 8 && t < 16) sm100::trace_event(args.trace, 4 * 512 + (warp * 8 + (t - 8)) * 8 + (e), 6 * 512)
+#define BWD_TR(e) if (lane == 0 && t >= 40 && t < 48) sm100::trace_event(args.trace, 4 * 512 + (warp * 8 + (t - 40)) * 8 + (e), 6 * 512)
           BWD_TR(qh == 0 ? 0 : 3);
           sm100::tc_fence_after();
           const uint32_t s_col = C::kColS + qh * 64 + w4 * 16, dp_col = C::kColDP + qh * 64 + w4 * 16;
@@ -496,14 +497,20 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
     const float alpha = args.scale;
     // dQ(tq) += alpha * TMEM dQ through the TMA: the fp32 tile is written (SW128, two 32-column
-    // boxes) into the dS buffer dQ(tq) has just finished reading, then one thread issues two bulk
-    // tensor reduce-adds into the fp32 accumulator (the adds happen in L2; no per-lane atomics).
+    // boxes) into a dedicated staging buffer, then one thread issues two bulk tensor reduce-adds
+    // into the fp32 accumulator (the adds happen in L2; no per-lane atomics).  (Reusing the dS
+    // buffer instead put the reduce's smem read on the dS staging path: +2000 clk per tile.)
     constexpr uint32_t kEpiThread0 = 32 * kComputeWarps;
+#define EPI_TR(tt, e) if (threadIdx.x == kEpiThread0 && (tt) >= 40 && (tt) < 48) sm100::trace_event(args.trace, 3072 + ((tt) - 40) * 16 + (e), 4094)
     auto drain_dq = [&](uint32_t tq, int zh, int i) {
       sm100::mbar_wait(dq_full, tq & 1);
+      EPI_TR(tq + 1, 7);
       sm100::tc_fence_after();
-      uint8_t* buf = smem + C::kDSOff + (tq & 1) * C::kDSBytes;
+      uint8_t* buf = smem + C::kDQOff;
       const uint32_t sb = sm100::smem_u32(buf) + row * 128;
+      // the previous tile's reduce-add has finished reading the staging buffer
+      if (threadIdx.x == kEpiThread0) sm100::bulk_wait_group_read<0>();
+      sm100::named_bar_sync(1, 128);
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {     // columns [32 hh, 32 hh + 32) -> box hh
         float r[2][16];
@@ -519,6 +526,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::tc_fence_before();
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(dq_empty);
+          EPI_TR(tq + 1, 8);
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c)   // 16-byte chunk c (columns 4c..4c+3) at slot c ^ (row & 7)
@@ -530,12 +538,14 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       sm100::fence_proxy_async_smem();
       sm100::named_bar_sync(1, 128);
+      EPI_TR(tq + 1, 9);
       if (threadIdx.x == kEpiThread0 && !SIGATTN_DBG_NORED) {
         // rows past Nq are clipped by the TMA; padded query rows add exact zeros (dS = 0 there)
         sm100::tma_reduce_add_3d(&tmDQ, buf, 0, i * kTile, zh);
         sm100::tma_reduce_add_3d(&tmDQ, buf + kTile * 128, 32, i * kTile, zh);
         sm100::bulk_commit_group();
       }
+      EPI_TR(tq + 1, 10);
     };
     uint32_t t = 0, item_c = 0;
     bool pend = false;            // a dQ tile waiting to be drained
@@ -552,6 +562,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll 1
         for (int qh = 0; qh < 2; ++qh) {
           sm100::mbar_wait(&p_full[qh], t & 1);
+          EPI_TR(t, qh == 0 ? 0 : 4);
           sm100::tc_fence_after();
           uint32_t d[4][8];   // packed dS^T of queries [64 qh + 16 g, +16) at columns 64 qh + 16 g + [0, 8)
 #pragma unroll
@@ -561,10 +572,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::tc_fence_before();
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&ds_copied[qh]);
+          EPI_TR(t, qh == 0 ? 1 : 5);
           if (qh == 0) {
             sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) MMA done with the buffer
-            if (threadIdx.x == kEpiThread0) sm100::bulk_wait_group_read<0>();   // ... and its reduce-add
-            sm100::named_bar_sync(1, 128);
+            EPI_TR(t, 2);
           }
 #pragma unroll
           for (int c = 0; c < 8 * !SIGATTN_DBG_NOSTAGE; ++c)   // 16-byte chunk c = queries [8c, 8c + 8) of this half, SW128 swizzle
@@ -573,6 +584,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&ds_full[t & 1]);
+          EPI_TR(t, qh == 0 ? 3 : 6);
           // SIGATTN_BWD_DRAIN_EARLY: drain dQ(t-1) between the two halves of tile t
           if (SIGATTN_BWD_DRAIN_EARLY && qh == 0 && pend) drain_dq(t - 1, pend_zh, pend_i);
         }
