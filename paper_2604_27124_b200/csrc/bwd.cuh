@@ -43,9 +43,6 @@
 #else
 #define MMA_WAIT_P(b, p) sm100::mbar_wait_backoff(b, p)
 #endif
-#ifndef SIGATTN_BWD_DRAIN_EARLY
-#define SIGATTN_BWD_DRAIN_EARLY 0
-#endif
 #ifndef SIGATTN_BWD_DQ_LATE
 #define SIGATTN_BWD_DQ_LATE 0
 #endif
@@ -199,7 +196,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&p_full[i], kComputeWarps);       // every compute warp works on every half
       sm100::mbar_init(&ds_copied[i], 4);
-      sm100::mbar_init(&ds_full[i], 8);                  // 4 epilogue warps x 2 halves
+      sm100::mbar_init(&ds_full[i], 4);                  // the 4 epilogue warps, after both halves
     }
     for (int i = 0; i < C::kQStages; ++i) {
       sm100::mbar_init(&qdo_full[i], 1);
@@ -581,14 +578,14 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           for (int c = 0; c < 8 * !SIGATTN_DBG_NOSTAGE; ++c)   // 16-byte chunk c = queries [8c, 8c + 8) of this half, SW128 swizzle
             sm100::st_shared_v4(dsr + qh * (kTile * 128) + ((c ^ (row & 7)) * 16), d[c >> 1][(c & 1) * 4],
                                 d[c >> 1][(c & 1) * 4 + 1], d[c >> 1][(c & 1) * 4 + 2], d[c >> 1][(c & 1) * 4 + 3]);
-          sm100::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&ds_full[t & 1]);
+          if (qh == 1) {   // one proxy fence covers both halves' stores
+            sm100::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&ds_full[t & 1]);
+          }
           EPI_TR(t, qh == 0 ? 3 : 6);
-          // SIGATTN_BWD_DRAIN_EARLY: drain dQ(t-1) between the two halves of tile t
-          if (SIGATTN_BWD_DRAIN_EARLY && qh == 0 && pend) drain_dq(t - 1, pend_zh, pend_i);
         }
-        if (!SIGATTN_BWD_DRAIN_EARLY && pend) drain_dq(t - 1, pend_zh, pend_i);
+        if (pend) drain_dq(t - 1, pend_zh, pend_i);
         pend = true;
         pend_zh = (int)zh;
         pend_i = i;
