@@ -64,8 +64,14 @@
 #ifndef SIGATTN_DBG_MMAONLY
 #define SIGATTN_DBG_MMAONLY 0     // timing experiments only: MMA + TMA pipeline alone (no compute/epilogue waits)
 #endif
+#ifndef SIGATTN_BWD_DQ2
+#define SIGATTN_BWD_DQ2 0         // 1: two TMEM dQ accumulators (uses the K/V columns: implies SCORES_SS)
+#endif
 #ifndef SIGATTN_BWD_SCORES_SS
-#define SIGATTN_BWD_SCORES_SS 0   // 1: S^T / dP^T MMAs read K / V from shared memory instead of TMEM
+#define SIGATTN_BWD_SCORES_SS SIGATTN_BWD_DQ2   // 1: S^T / dP^T MMAs read K / V from smem, not TMEM
+#endif
+#if SIGATTN_BWD_DQ2 && !SIGATTN_BWD_SCORES_SS
+#error "SIGATTN_BWD_DQ2 needs SIGATTN_BWD_SCORES_SS"
 #endif
 
 namespace sigattn {
@@ -98,7 +104,8 @@ struct BwdCfg {
   static constexpr int kDSBytes = 2 * kTile * 128;
   static constexpr int kDQOff = kDSOff + 2 * kDSBytes;      // fp32 dQ staging tile for the TMA reduce-add
   static constexpr int kBarOff = kDQOff + kTile * D * 4;
-  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1 + 2 + 2;
+  static constexpr int kDQBufs = SIGATTN_BWD_DQ2 ? 2 : 1;   // TMEM dQ accumulators
+  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 2 * kDQBufs + 1 + 1 + 2 + 2;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kNumWG = 4;                           // compute warpgroups
   static constexpr int kWarpEpi = 4 * kNumWG, kWarpTMA = kWarpEpi + 4, kWarpMMA = kWarpTMA + 1,
@@ -176,9 +183,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* s_full = qdo_empty + C::kQStages;     // [2] per query half: S^T, dP^T in TMEM
   uint64_t* p_full = s_full + 2;                  // [2] per query half: P^T, dS^T in TMEM, dS^T in smem
   uint64_t* ds_free = p_full + 2;                 // [2] dQ MMA finished reading dS^T buffer
-  uint64_t* dq_full = ds_free + 2;
-  uint64_t* dq_empty = dq_full + 1;
-  uint64_t* acc_full = dq_empty + 1;
+  uint64_t* dq_full = ds_free + 2;                // [kDQBufs]
+  uint64_t* dq_empty = dq_full + C::kDQBufs;      // [kDQBufs]
+  uint64_t* acc_full = dq_empty + C::kDQBufs;
   uint64_t* acc_empty = acc_full + 1;
   uint64_t* ds_copied = acc_empty + 1;            // [2] per query half: epilogue read dS^T from TMEM
   uint64_t* ds_full = ds_copied + 2;              // [2] per dS smem buffer: both halves staged + fenced
@@ -202,8 +209,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&qdo_full[i], 1);
       sm100::mbar_init(&qdo_empty[i], 1);
     }
-    sm100::mbar_init(dq_full, 1);
-    sm100::mbar_init(dq_empty, 4);
+    for (int i = 0; i < C::kDQBufs; ++i) {
+      sm100::mbar_init(&dq_full[i], 1);
+      sm100::mbar_init(&dq_empty[i], 4);
+    }
     sm100::mbar_init(acc_full, 1);
     sm100::mbar_init(acc_empty, 4);
     sm100::fence_barrier_init();
@@ -325,7 +334,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_wait(&qdo_full[0], 0);
       sm100::tc_fence_after();
       if (sm100::elect_one()) {
-        copy_kv(cur.item_c & 1);
+        if (!SIGATTN_BWD_SCORES_SS) copy_kv(cur.item_c & 1);
         mma1(cur.item_c & 1, 0, 0);
         mma1(cur.item_c & 1, 0, 1);
       }
@@ -338,7 +347,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     auto issue_dq = [&](uint32_t tq) {
       const uint32_t b2 = tq & 1;
 #if !SIGATTN_DBG_MMAONLY
-      sm100::mbar_wait(dq_empty, (tq & 1) ^ 1);                  // epilogue drained dQ(tq-1)
+      const uint32_t qb = tq % C::kDQBufs;
+      sm100::mbar_wait(&dq_empty[qb], ((tq / C::kDQBufs) & 1) ^ 1);   // epilogue drained this accumulator
       sm100::mbar_wait(&ds_full[b2], (tq >> 1) & 1);             // dS(tq) staged in smem, proxy-fenced
 #endif
       sm100::tc_fence_after();
@@ -348,10 +358,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         // dQ = dS K   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major, B = K MN-major)
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk)
-          sm100::mma_ss(tmem + C::kColDQ, sm100::make_sdesc_sw128(dsa + kk * 2048, kTile * 128, 1024),
+          sm100::mma_ss(tmem + C::kColDQ + qb * 64, sm100::make_sdesc_sw128(dsa + kk * 2048, kTile * 128, 1024),
                         sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024), idesc_dq, kk > 0);
         sm100::mma_commit(&ds_free[b2]);
-        sm100::mma_commit(dq_full);
+        sm100::mma_commit(&dq_full[qb]);
         if (prev_last) sm100::mma_commit(&kv_empty[prev_kvb]);   // K/V smem slot free
       }
       __syncwarp();
@@ -383,7 +393,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (sm100::elect_one()) {
           // the copy executes after every earlier MMA (tcgen05 ops of one thread run in order), so
           // S/dP(i, q1) has finished reading the previous K/V columns
-          if (nxt.i == 0) copy_kv(nxt.item_c & 1);
+          if (!SIGATTN_BWD_SCORES_SS && nxt.i == 0) copy_kv(nxt.item_c & 1);
           mma1(nxt.item_c & 1, st1, 0);
         }
         __syncwarp();
@@ -500,7 +510,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     constexpr uint32_t kEpiThread0 = 32 * kComputeWarps;
 #define EPI_TR(tt, e) if (threadIdx.x == kEpiThread0 && (tt) >= 40 && (tt) < 48) sm100::trace_event(args.trace, 3072 + ((tt) - 40) * 16 + (e), 4094)
     auto drain_dq = [&](uint32_t tq, int zh, int i) {
-      sm100::mbar_wait(dq_full, tq & 1);
+      const uint32_t qb = tq % C::kDQBufs;
+      sm100::mbar_wait(&dq_full[qb], (tq / C::kDQBufs) & 1);
       EPI_TR(tq + 1, 7);
       sm100::tc_fence_after();
       uint8_t* buf = smem + C::kDQOff;
@@ -512,17 +523,17 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       for (int hh = 0; hh < 2; ++hh) {     // columns [32 hh, 32 hh + 32) -> box hh
         float r[2][16];
         if (SIGATTN_DBG_EPI_NOLD) {
-          if (hh == 1 && lane == 0) sm100::mbar_arrive(dq_empty);
+          if (hh == 1 && lane == 0) sm100::mbar_arrive(&dq_empty[qb]);
           continue;
         }
-        sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + hh * 32, r[0]);
-        sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + hh * 32 + 16, r[1]);
+        sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + qb * 64 + hh * 32, r[0]);
+        sm100::tmem_ld16(tmem + lane_addr + C::kColDQ + qb * 64 + hh * 32 + 16, r[1]);
         sm100::tmem_wait_ld_dep16(r[0]);
         sm100::tmem_wait_ld_dep16(r[1]);
         if (hh == 1) {
           sm100::tc_fence_before();
           __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(dq_empty);
+          if (lane == 0) sm100::mbar_arrive(&dq_empty[qb]);
           EPI_TR(tq + 1, 8);
         }
 #pragma unroll
