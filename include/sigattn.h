@@ -48,6 +48,10 @@ typedef enum {
 
 /* flags bitfield */
 enum {
+  SIGATTN_F_BWD_DETERMINISTIC = 1u << 0, /* bwd: the paper's two-pass split -- a query-tile-owned
+                                          dQ pass (Alg. 2) + a key-tile-owned dK/dV
+                                          pass (Alg. 3).  No atomics: bitwise
+                                          reproducible dQ; 14d instead of 10d FLOP per pair.  */
   SIGATTN_F_OUT_F32_PARTIAL = 1u << 1, /* fwd: o is float* (fp32, no cast) -- a partial O
                                           for key-split context parallelism (A4)     */
   SIGATTN_F_DQ_F32_PARTIAL = 1u << 2,  /* bwd: dq is float* fp32 alpha*dS K, not finalised
@@ -78,7 +82,8 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
 size_t sigattn_bwd_workspace_bytes(const sigattn_params* p);
 
 /* Backward (Alg. 2 + Alg. 3, fused into one key-tile-owned pass: dK/dV accumulate on chip
- * without atomics, dQ partials are reduced into the fp32 workspace, then finalised).
+ * without atomics, dQ partials are reduced into the fp32 workspace, then finalised; with
+ * SIGATTN_F_BWD_DETERMINISTIC the paper's two passes run instead, see above).
  * dout [B,H,Nq,d]; dq [B,H,Nq,d] (fp32 if DQ_F32_PARTIAL); dk, dv [B,H,Nk,d].
  * workspace: device, >= sigattn_bwd_workspace_bytes(p), 16-byte aligned, caller-owned.       */
 sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k, const void* v,

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(PKG, "libsigattn.so")
 SIGATTN_BF16 = 0
 SIGATTN_FP16 = 1
 SIGATTN_OK = 0
+SIGATTN_F_BWD_DETERMINISTIC = 1 << 0
 SIGATTN_F_OUT_F32_PARTIAL = 1 << 1
 SIGATTN_F_DQ_F32_PARTIAL = 1 << 2
 SIGATTN_F_NO_ZERO_PAD_OUT = 1 << 3

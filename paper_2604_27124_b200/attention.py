@@ -111,8 +111,13 @@ def bwd_workspace_bytes(B, H, Nq, Nk, d, dtype=torch.bfloat16) -> int:
 
 
 def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias: BiasArg = None,
-                dq=None, dk=None, dv=None, workspace: Optional[torch.Tensor] = None, dq_f32: bool = False):
-    """Backward (Alg. 2 + Alg. 3, fused).  Returns (dQ, dK, dV); dQ is fp32 if dq_f32 (CP partial)."""
+                dq=None, dk=None, dv=None, workspace: Optional[torch.Tensor] = None, dq_f32: bool = False,
+                deterministic: bool = False):
+    """Backward (Alg. 2 + Alg. 3, fused).  Returns (dQ, dK, dV); dQ is fp32 if dq_f32 (CP partial).
+
+    deterministic=True runs the paper's two passes instead (dK/dV key-tile-owned, dQ
+    query-tile-owned): no atomics, bitwise reproducible, ~40% more tensor work.
+    """
     lib = _lib.load()
     B, H, Nq, Nk, d = _check_qkv(q, k, v)
     if dout.shape != q.shape or dout.dtype != q.dtype or not dout.is_contiguous():
@@ -124,7 +129,7 @@ def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias:
     dq = torch.empty((B, H, Nq, d), dtype=torch.float32 if dq_f32 else q.dtype, device=q.device) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
-    flags = _lib.SIGATTN_F_DQ_F32_PARTIAL if dq_f32 else 0
+    flags = (_lib.SIGATTN_F_DQ_F32_PARTIAL if dq_f32 else 0) | (_lib.SIGATTN_F_BWD_DETERMINISTIC if deterministic else 0)
     p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags)
     need = int(lib.sigattn_bwd_workspace_bytes(ctypes.byref(p)))
     if workspace is None or workspace.numel() * workspace.element_size() < need:
@@ -178,24 +183,28 @@ class SigmoidAttentionFn(torch.autograd.Function):
     """Autograd op: saves q, k, v and the lengths -- never O or P (P is recomputed)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, seqlens_q, seqlens_k, scale, bias):
+    def forward(ctx, q, k, v, seqlens_q, seqlens_k, scale, bias, deterministic=False):
         o = sigattn_fwd(q, k, v, seqlens_q, seqlens_k, scale, bias)
         ctx.save_for_backward(q, k, v, seqlens_q, seqlens_k, bias if isinstance(bias, torch.Tensor) else None)
         ctx.scale = scale
         ctx.bias = None if isinstance(bias, torch.Tensor) else bias
+        ctx.deterministic = deterministic
         return o
 
     @staticmethod
     def backward(ctx, do):
         q, k, v, sq, sk, bt = ctx.saved_tensors
         bias = bt if bt is not None else ctx.bias
-        dq, dk, dv = sigattn_bwd(q, k, v, do.contiguous(), sq, sk, ctx.scale, bias)
-        return dq, dk, dv, None, None, None, None
+        dq, dk, dv = sigattn_bwd(q, k, v, do.contiguous(), sq, sk, ctx.scale, bias,
+                                 deterministic=ctx.deterministic)
+        return dq, dk, dv, None, None, None, None, None
 
 
 def sigmoid_attention(q, k, v, seqlens_q=None, seqlens_k=None, key_padding_mask=None,
-                      scale: Optional[float] = None, bias: BiasArg = None):
+                      scale: Optional[float] = None, bias: BiasArg = None, deterministic: bool = False):
     """O = sigma(scale * Q K^T + bias) V with padded keys at zero weight; differentiable.
+
+    deterministic=True selects the paper's two-pass backward (bitwise reproducible dQ).
 
     q [B,H,Nq,d], k/v [B,H,Nk,d] (bf16/fp16, CUDA, contiguous).  Lengths as int32 [B] tensors,
     or a PyTorch key_padding_mask [B, Nk] (True = pad; prefix masks only).
@@ -211,4 +220,4 @@ def sigmoid_attention(q, k, v, seqlens_q=None, seqlens_k=None, key_padding_mask=
     sk = _lens(seqlens_k, B, q.device)
     if sk is None and sq is not None and q.shape[2] == k.shape[2]:
         sk = sq
-    return SigmoidAttentionFn.apply(q, k, v, sq, sk, scale, bias)
+    return SigmoidAttentionFn.apply(q, k, v, sq, sk, scale, bias, deterministic)

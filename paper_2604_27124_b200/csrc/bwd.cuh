@@ -167,7 +167,9 @@ __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16],
   }
 }
 
-template <int D, bool kBf16>
+// kDQ = false: dK, dV only (the key-tile-owned pass of the deterministic backward, Alg. 3;
+// dQ then comes from sigattn_dq_kernel, Alg. 2): no dQ MMA, no dS staging, no dQ reduction.
+template <int D, bool kBf16, bool kDQ = true>
 __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
 sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -345,6 +347,11 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     uint32_t prev_kvb = 0;
     bool prev_last = false;      // the tile dQ is pending for was its item's last (frees its K/V slot)
     auto issue_dq = [&](uint32_t tq) {
+      if constexpr (!kDQ) {
+        if (sm100::elect_one() && prev_last) sm100::mma_commit(&kv_empty[prev_kvb]);   // K/V smem slot free
+        __syncwarp();
+        return;
+      }
       const uint32_t b2 = tq & 1;
 #if !SIGATTN_DBG_MMAONLY
       const uint32_t qb = tq % C::kDQBufs;
@@ -387,7 +394,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
         sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
 #if !SIGATTN_DBG_MMAONLY
-        sm100::mbar_wait(&ds_copied[0], t & 1);      // dS^T(t, q0) left TMEM before S/dP(t+1, q0) land there
+        if (kDQ) sm100::mbar_wait(&ds_copied[0], t & 1);   // dS^T(t, q0) left TMEM before S/dP(t+1, q0) land there
 #endif
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
@@ -415,7 +422,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       __syncwarp();
       if (nxt.valid) {
 #if !SIGATTN_DBG_MMAONLY
-        sm100::mbar_wait(&ds_copied[1], t & 1);
+        if (kDQ) sm100::mbar_wait(&ds_copied[1], t & 1);
 #endif
         sm100::tc_fence_after();
         if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 1);
@@ -565,7 +572,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const size_t zh = (size_t)(b * args.H + h);
-      for (int i = 0; i < nqt; ++i, ++t) {
+      for (int i = 0; i < nqt * kDQ; ++i, ++t) {
         const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
 #pragma unroll 1
         for (int qh = 0; qh < 2; ++qh) {
@@ -645,8 +652,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       ++item_c;
     }
-    if (pend) drain_dq(t - 1, pend_zh, pend_i);
-    if (threadIdx.x == kEpiThread0) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
+    if (kDQ && pend) drain_dq(t - 1, pend_zh, pend_i);
+    if (kDQ && threadIdx.x == kEpiThread0) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
   }
 
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes

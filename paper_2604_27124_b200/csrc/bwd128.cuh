@@ -42,7 +42,8 @@ struct Bwd128Cfg {
   static constexpr uint32_t kColS = 0, kColDP = 64, kColDV = 128, kColDK = 256, kColDQ = 384;
 };
 
-template <bool kBf16>
+// kDQ = false: dK, dV only (deterministic backward, Alg. 3); see bwd.cuh.
+template <bool kBf16, bool kDQ = true>
 __global__ void __launch_bounds__(Bwd128Cfg::kThreads, 1)
 sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -216,13 +217,17 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
           if (sm100::elect_one()) mma_s(st1);
           __syncwarp();
         }
-        sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) {
-          mma_dq(buf);
-          sm100::mma_commit(&ds_free[buf]);
-          sm100::mma_commit(dq_full);
-          if (i == nqt - 1) sm100::mma_commit(kv_empty);
+        if constexpr (kDQ) {
+          sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
+          sm100::tc_fence_after();
+          if (sm100::elect_one()) {
+            mma_dq(buf);
+            sm100::mma_commit(&ds_free[buf]);
+            sm100::mma_commit(dq_full);
+            if (i == nqt - 1) sm100::mma_commit(kv_empty);
+          }
+        } else {
+          if (sm100::elect_one() && i == nqt - 1) sm100::mma_commit(kv_empty);
         }
         __syncwarp();
       }
@@ -251,7 +256,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       for (int i = 0; i < nqt; ++i, ++t) {
         sm100::mbar_wait(s_full, t & 1);
-        sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
+        if (kDQ) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
         float s[16], dp[16];
         sm100::tmem_ld16(tmem + lane_addr + s_col, s);
@@ -264,14 +269,16 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
         sm100::tmem_st8(tmem + lane_addr + s_col, pp);
         sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
-        const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
+        if constexpr (kDQ) {
+          const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const uint32_t chunk = (uint32_t)(w4 * 2 + u) ^ (row & 7);
-          sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t chunk = (uint32_t)(w4 * 2 + u) ^ (row & 7);
+            sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+          }
         }
         sm100::tmem_wait_st();
-        sm100::fence_proxy_async_smem();
+        if (kDQ) sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(p_full);
@@ -291,7 +298,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const size_t zh = (size_t)(b * args.H + h);
-      for (int i = 0; i < nqt; ++i, ++t) {
+      for (int i = 0; i < nqt * kDQ; ++i, ++t) {
         sm100::mbar_wait_backoff(dq_full, t & 1);
         sm100::tc_fence_after();
         float r[4][16];

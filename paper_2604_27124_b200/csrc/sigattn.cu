@@ -16,6 +16,7 @@
 #include "../../include/sigattn.h"
 #include "bwd.cuh"
 #include "bwd128.cuh"
+#include "dq.cuh"
 #include "fwd.cuh"
 #include "sched.cuh"
 
@@ -177,7 +178,7 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   return SIGATTN_OK;
 }
 
-template <int D, bool kBf16>
+template <int D, bool kBf16, bool kDQ = true>
 sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                           float* dq_acc, void* dk, void* dv,
                           const int4* items, const int* n_items, int max_items, cudaStream_t s) {
@@ -190,7 +191,9 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
   if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
   CUtensorMap tdq;   // fp32 dQ accumulator, 32-column boxes for the TMA reduce-add
-  if ((st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  std::memset(&tdq, 0, sizeof(tdq));
+  if (kDQ && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, bh)) != SIGATTN_OK)
+    return st;
   BwdArgs a;
   a.items = items;
   a.n_items = n_items;
@@ -208,7 +211,7 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   a.dv = dv;
   a.trace = g_trace;
   using C = BwdCfg<D>;
-  auto kern = sigattn_bwd_kernel<D, kBf16>;
+  auto kern = sigattn_bwd_kernel<D, kBf16, kDQ>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);
@@ -219,7 +222,7 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   return SIGATTN_OK;
 }
 
-template <bool kBf16>
+template <bool kBf16, bool kDQ = true>
 sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                              float* dq_acc, void* dk, void* dv,
                              const int4* items, const int* n_items, int max_items, cudaStream_t s) {
@@ -247,12 +250,46 @@ sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void*
   a.dk = dk;
   a.dv = dv;
   a.trace = g_trace;
-  auto kern = sigattn_bwd128_kernel<kBf16>;
+  auto kern = sigattn_bwd128_kernel<kBf16, kDQ>;
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);
   kern<<<grid, Bwd128Cfg::kThreads, Bwd128Cfg::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
   prof_record(3, s);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+template <int D, bool kBf16, bool kF32>
+sigattn_status launch_dq(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
+                         void* dq, const int4* items, const int* n_items, int max_items, cudaStream_t s) {
+  const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tq, tk, tv, tdo;
+  const int bh = p->B * p->H;
+  sigattn_status st;
+  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  DqArgs a;
+  a.items = items;
+  a.n_items = n_items;
+  a.seqlens_q = p->seqlens_q;
+  a.seqlens_k = p->seqlens_k;
+  a.bias_per_seq = p->bias_per_seq;
+  a.bias = p->bias;
+  a.scale = p->scale;
+  a.B = p->B;
+  a.H = p->H;
+  a.Nq = p->Nq;
+  a.Nk = p->Nk;
+  a.dq = dq;
+  using C = DqCfg<D>;
+  auto kern = sigattn_dq_kernel<D, kBf16, kF32>;
+  if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
+  const int grid = std::max(1, std::min(num_sms(), max_items));
+  kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
@@ -286,6 +323,9 @@ sigattn_status get_scratch(cudaStream_t s, size_t bytes, void** out) {
 size_t ws_acc_bytes(const sigattn_params* p) { return align_up((size_t)p->B * p->H * p->Nq * p->d * sizeof(float), 256); }
 size_t ws_items_bytes(const sigattn_params* p) {
   return align_up(16 + (size_t)p->B * p->H * cdiv(p->Nk, 128) * sizeof(int4), 256);
+}
+size_t ws_items_q_bytes(const sigattn_params* p) {   // query-tile work list (deterministic dQ pass)
+  return align_up(16 + (size_t)p->B * p->H * cdiv(p->Nq, 128) * sizeof(int4), 256);
 }
 
 }  // namespace
@@ -384,6 +424,7 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
 
 size_t sigattn_bwd_workspace_bytes(const sigattn_params* p) {
   if (check_params(p) != SIGATTN_OK) return 0;
+  if (p->flags & SIGATTN_F_BWD_DETERMINISTIC) return ws_items_bytes(p) + ws_items_q_bytes(p);
   return ws_acc_bytes(p) + ws_items_bytes(p);
 }
 
@@ -401,6 +442,37 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool dq_f32 = (p->flags & SIGATTN_F_DQ_F32_PARTIAL) != 0;
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  const bool bf = p->dtype == SIGATTN_BF16;
+  if (p->flags & SIGATTN_F_BWD_DETERMINISTIC) {
+    // Alg. 3 (dK, dV; key-tile-owned) then Alg. 2 (dQ; query-tile-owned) -- no atomics anywhere
+    int* n_items = reinterpret_cast<int*>(ws);
+    int4* items = reinterpret_cast<int4*>(ws + 16);
+    int* nq_items = reinterpret_cast<int*>(ws + ws_items_bytes(p));
+    int4* q_items = reinterpret_cast<int4*>(ws + ws_items_bytes(p) + 16);
+    if ((st = launch_bwd_prep(p, items, n_items, nullptr, s)) != SIGATTN_OK) return st;
+    const int max_items = p->B * p->H * cdiv(p->Nk, 128);
+    if (p->d == 64)
+      st = bf ? launch_bwd<64, true, false>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s)
+              : launch_bwd<64, false, false>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s);
+    else
+      st = bf ? launch_bwd128<true, false>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s)
+              : launch_bwd128<false, false>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s);
+    if (st != SIGATTN_OK) return st;
+    if ((st = launch_worklist(0, p, q_items, nq_items, s)) != SIGATTN_OK) return st;
+    const int max_q_items = p->B * p->H * cdiv(p->Nq, 128);
+    if (p->d == 64) {
+      if (bf) st = dq_f32 ? launch_dq<64, true, true>(p, q, k, v, dout, dq, q_items, nq_items, max_q_items, s)
+                          : launch_dq<64, true, false>(p, q, k, v, dout, dq, q_items, nq_items, max_q_items, s);
+      else st = dq_f32 ? launch_dq<64, false, true>(p, q, k, v, dout, dq, q_items, nq_items, max_q_items, s)
+                       : launch_dq<64, false, false>(p, q, k, v, dout, dq, q_items, nq_items, max_q_items, s);
+    } else {
+      if (bf) st = dq_f32 ? launch_dq<128, true, true>(p, q, k, v, dout, dq, q_items, nq_items, max_q_items, s)
+                          : launch_dq<128, true, false>(p, q, k, v, dout, dq, q_items, nq_items, max_q_items, s);
+      else st = dq_f32 ? launch_dq<128, false, true>(p, q, k, v, dout, dq, q_items, nq_items, max_q_items, s)
+                       : launch_dq<128, false, false>(p, q, k, v, dout, dq, q_items, nq_items, max_q_items, s);
+    }
+    return st;
+  }
   const size_t acc_bytes = ws_acc_bytes(p);
   float* dq_acc = dq_f32 ? reinterpret_cast<float*>(dq) : reinterpret_cast<float*>(ws);
   int* n_items = reinterpret_cast<int*>(ws + acc_bytes);
@@ -410,7 +482,6 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   if (dq_f32) CUDA_TRY(cudaMemsetAsync(dq, 0, (size_t)p->B * p->H * p->Nq * p->d * sizeof(float), s));
   if ((st = launch_bwd_prep(p, items, n_items, dq_f32 ? nullptr : dq_acc, s)) != SIGATTN_OK)
     return st;
-  const bool bf = p->dtype == SIGATTN_BF16;
   if (p->d == 64)
     st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
                                    max_items, s)

@@ -34,7 +34,7 @@ def relerr(got, ref):
     return float(np.abs(got - ref).max() / den)
 
 
-def run_case(cfg, bias=None, check_bwd=True, pad=None, tol=BF16_TOL, nan_prefill=False):
+def run_case(cfg, bias=None, check_bwd=True, pad=None, tol=BF16_TOL, nan_prefill=False, deterministic=False):
     """nan_prefill: outputs are preallocated full of NaN, so every element (padded rows included)
     must be written by the kernels (the pad fill runs inside the attention kernels)."""
     sa = _sa()
@@ -52,7 +52,8 @@ def run_case(cfg, bias=None, check_bwd=True, pad=None, tol=BF16_TOL, nan_prefill
         assert torch.all(o[bb, :, cfg.nq[bb]:] == 0), "padded query rows must be exactly 0"
     res = {"o": e}
     if check_bwd:
-        dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b, dq=nan(q), dk=nan(k), dv=nan(v))
+        dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b, dq=nan(q), dk=nan(k), dv=nan(v),
+                                    deterministic=deterministic)
         torch.cuda.synchronize()
         rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, alpha, bias_np)
         for name, got, ref in (("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
@@ -297,3 +298,47 @@ def test_cp_autograd_world1_nccl():
     finally:
         if created:
             dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------------------
+# deterministic backward: the paper's Alg. 2 (query-tile-owned dQ) + Alg. 3 (key-tile-owned dK/dV)
+@pytest.mark.parametrize("cfg", [
+    I.C1,
+    I.C1_FP16,
+    I.Config("det_ragged", B=5, H=2, N=300, d=64, lengths=[300, 1, 129, 0, 256], seed=30),
+    I.Config("det_cross", B=3, H=2, N=320, d=64, lengths=[320, 0, 7], Nk=200, lengths_k=[200, 150, 0], seed=31),
+    I.Config("det_d128", B=4, H=2, N=300, d=128, lengths=[300, 65, 0, 128], seed=32),
+    I.Config("det_d128_cross", B=3, H=2, N=200, d=128, lengths=[200, 63, 9], Nk=330, lengths_k=[0, 330, 129], seed=33),
+])
+def test_deterministic_backward_parity(cfg):
+    run_case(cfg, nan_prefill=True, deterministic=True, tol=FP16_FWD_TOL if cfg.dtype == "fp16" else BF16_TOL)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_deterministic_backward_bitwise(d):
+    """Same inputs twice -> bitwise identical dQ, dK, dV; dK/dV also equal the fused kernel's."""
+    sa = _sa()
+    cfg = I.Config("det_bits", B=4, H=3, N=640, d=d, lengths=[640, 333, 129, 500], seed=34)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    r1 = sa.sigattn_bwd(q, k, v, do, nq, nk, deterministic=True)
+    r2 = sa.sigattn_bwd(q, k, v, do, nq, nk, deterministic=True)
+    rf = sa.sigattn_bwd(q, k, v, do, nq, nk)
+    torch.cuda.synchronize()
+    for a, b_ in zip(r1, r2):
+        assert torch.equal(a, b_)
+    assert torch.equal(r1[1], rf[1]) and torch.equal(r1[2], rf[2])   # dK, dV: same arithmetic
+    assert relerr(f64(r1[0]), f64(rf[0])) < 1e-2
+
+
+def test_deterministic_autograd():
+    sa = _sa()
+    cfg = I.Config("det_ag", B=2, H=2, N=256, d=64, lengths=[256, 100], seed=35)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    grads = []
+    for det in (False, True):
+        qq, kk, vv = (t.clone().requires_grad_(True) for t in (q, k, v))
+        o = sa.sigmoid_attention(qq, kk, vv, seqlens_q=nq, seqlens_k=nk, deterministic=det)
+        o.backward(do)
+        grads.append((qq.grad, kk.grad, vv.grad))
+    assert torch.equal(grads[0][1], grads[1][1]) and torch.equal(grads[0][2], grads[1][2])
+    assert relerr(f64(grads[1][0]), f64(grads[0][0])) < 1e-2
