@@ -353,8 +353,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         return;
       }
       const uint32_t b2 = tq & 1;
-#if !SIGATTN_DBG_MMAONLY
       const uint32_t qb = tq % C::kDQBufs;
+#if !SIGATTN_DBG_MMAONLY
       sm100::mbar_wait(&dq_empty[qb], ((tq / C::kDQBufs) & 1) ^ 1);   // epilogue drained this accumulator
       sm100::mbar_wait(&ds_full[b2], (tq >> 1) & 1);             // dS(tq) staged in smem, proxy-fenced
 #endif

@@ -21,6 +21,9 @@
 #include "sigmoid.cuh"
 #include "sm100.cuh"
 
+#ifndef SIGATTN_DBG_FWD_NOSIGMA
+#define SIGATTN_DBG_FWD_NOSIGMA 0
+#endif
 #ifndef SIGATTN_FWD_EMU
 #define SIGATTN_FWD_EMU 0   // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
 #endif
@@ -296,8 +299,13 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           float r[32];
           uint32_t pk[16];
           sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+#if SIGATTN_DBG_FWD_NOSIGMA   // timing experiments only: P = bits of S, no sigma work
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[e] = __float_as_uint(r[2 * e]) ^ __float_as_uint(r[2 * e + 1]);
+#else
           if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
           else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+#endif
           // P over the first half of this warpgroup's 64 columns (chunk 0's columns are already read)
           sm100::tmem_st16(tmem + lane_addr + (si % C::kSBuf) * 128 + gp * 64 + ch * 16, pk);
         }
