@@ -88,6 +88,7 @@ struct BwdArgs {
   float* dq_acc;          // fp32 [B,H,Nq,D], zero on valid rows at entry; receives alpha dS K
   void* dk;               // [B,H,Nk,D]
   void* dv;
+  void* dq_pad;           // 16-bit dQ output whose rows >= ceil128(n_q) the fill warp zeroes, or nullptr
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots (8 events x 512 tiles)
 };
 
@@ -659,6 +660,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
     pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
     pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
+    if (args.dq_pad)   // dq_finalize_kernel covers the rows below
+      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane);
   }
 
   sm100::tc_fence_before();

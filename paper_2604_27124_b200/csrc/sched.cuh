@@ -168,11 +168,14 @@ __device__ __forceinline__ void dq_finalize_rows(const float* __restrict__ acc, 
 // dq[b,h,i,:] = i < n_q[b] ? round(acc[b,h,i,:]) : 0    (acc already holds alpha * dS K)
 template <bool kBf16>
 __global__ void dq_finalize_kernel(const float* __restrict__ acc, uint16_t* __restrict__ dq, int H, int N, int D,
-                                   const int32_t* __restrict__ lens) {
+                                   const int32_t* __restrict__ lens, const int32_t* __restrict__ lens_k, int Nk) {
   const int zh = blockIdx.y;
-  const int nq = clamp_len(lens, zh / H, N);
-  const int rows = (N + gridDim.x - 1) / gridDim.x;
-  const int r0 = blockIdx.x * rows, r1 = min(N, r0 + rows);
+  const int nq = clamp_len(lens, zh / H, N), nk = clamp_len(lens_k, zh / H, Nk);
+  // rows from ceil128(n_q) on (all rows if the sequence has no work) are zeroed by the backward
+  // kernel's fill warp; finalise the rest
+  const int rlim = (nq == 0 || nk == 0) ? 0 : min((nq + 127) & ~127, N);
+  const int rows = (rlim + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * rows, r1 = min(rlim, r0 + rows);
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int per = (r1 - r0 + nwarps - 1) / nwarps;
   const int w0 = r0 + warp * per, w1 = min(r1, w0 + per);

@@ -181,7 +181,8 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
 template <int D, bool kBf16, bool kDQ = true>
 sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                           float* dq_acc, void* dk, void* dv,
-                          const int4* items, const int* n_items, int max_items, cudaStream_t s) {
+                          const int4* items, const int* n_items, int max_items, cudaStream_t s,
+                          void* dq_pad = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
   const int bh = p->B * p->H;
@@ -209,6 +210,7 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   a.dq_acc = dq_acc;
   a.dk = dk;
   a.dv = dv;
+  a.dq_pad = dq_pad;
   a.trace = g_trace;
   using C = BwdCfg<D>;
   auto kern = sigattn_bwd_kernel<D, kBf16, kDQ>;
@@ -225,7 +227,8 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
 template <bool kBf16, bool kDQ = true>
 sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                              float* dq_acc, void* dk, void* dv,
-                             const int4* items, const int* n_items, int max_items, cudaStream_t s) {
+                             const int4* items, const int* n_items, int max_items, cudaStream_t s,
+                             void* dq_pad = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
   const int bh = p->B * p->H;
@@ -249,6 +252,7 @@ sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void*
   a.dq_acc = dq_acc;
   a.dk = dk;
   a.dv = dv;
+  a.dq_pad = dq_pad;
   a.trace = g_trace;
   auto kern = sigattn_bwd128_kernel<kBf16, kDQ>;
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
@@ -482,24 +486,21 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   if (dq_f32) CUDA_TRY(cudaMemsetAsync(dq, 0, (size_t)p->B * p->H * p->Nq * p->d * sizeof(float), s));
   if ((st = launch_bwd_prep(p, items, n_items, dq_f32 ? nullptr : dq_acc, s)) != SIGATTN_OK)
     return st;
+  void* dq_pad = dq_f32 ? nullptr : dq;   // 16-bit dQ: the kernel's fill warp zeroes rows >= ceil128(n_q)
   if (p->d == 64)
-    st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
-                                   max_items, s)
-            : launch_bwd<64, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
-                                    max_items, s);
+    st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad)
+            : launch_bwd<64, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad);
   else
-    st = bf ? launch_bwd128<true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
-                                  max_items, s)
-            : launch_bwd128<false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items,
-                                   max_items, s);
+    st = bf ? launch_bwd128<true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad)
+            : launch_bwd128<false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad);
   if (st != SIGATTN_OK || dq_f32) return st;
-  const dim3 grid(std::max(1, std::min(32, cdiv(p->Nq, 256))), p->B * p->H);
+  const dim3 grid(std::max(1, std::min(32, cdiv(p->Nq, 512))), p->B * p->H);
   if (bf)
     dq_finalize_kernel<true><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
-                                                  p->seqlens_q);
+                                                  p->seqlens_q, p->seqlens_k, p->Nk);
   else
     dq_finalize_kernel<false><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
-                                                   p->seqlens_q);
+                                                   p->seqlens_q, p->seqlens_k, p->Nk);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
