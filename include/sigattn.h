@@ -102,7 +102,8 @@ int64_t sigattn_valid_flops(int B, int H, int d, const int32_t* host_nq, const i
                             int forward);
 
 /* Host mirror of the device work-list builder, for tests and schedulers: writes the items the
- * forward (kind = 0, items = (b,h,q-tile), cost = key tiles) or backward (kind = 1, items =
+ * forward (kind = 0, items = (b,h,q-tile), cost = key tiles; kind = 2, items = (b,h,pair of
+ * q-tiles 2t and 2t+1), cost = key tiles -- the two-tile forward) or backward (kind = 1, items =
  * (b,h,k-tile), cost = query tiles) kernel visits, in visiting order (longest first, ties by
  * b then h then tile).  Each item is 4 int32: {b, h, tile, cost}.  Returns the item count, or
  * -1 on bad arguments; writes at most max_items.  tile = 128 rows.                            */

@@ -1,0 +1,310 @@
+// fwd2.cuh -- forward kernel with two query tiles per CTA (Alg. 1).
+//
+// A work item is a PAIR of consecutive 128-query tiles (A = 2p, B = 2p + 1) of one (b, h); both
+// tiles walk the same key tiles, so K_j / V_j are loaded once for the two.  Each query tile has
+// its own S buffer (P aliased onto it) and its own O accumulator in TMEM, and its own warpgroup
+// pair of sigma warps:
+//   warps 0-7   pair A: sigma for tile A (warpgroup gp owns key columns [64 gp, +64), two chunks
+//               of 32; thread = query row = TMEM lane); then tile A's O epilogue
+//   warps 8-15  pair B: the same for tile B (idle when the sequence has an odd tile count)
+//   warp 16     TMA: the Q pair, then K_j / V_j rings
+//   warp 17     MMA: S_A(0), S_B(0); per key tile j: PV_A(j), S_A(j+1) as soon as P_A(j) is
+//               ready, then PV_B(j), S_B(j+1).  The two tiles' chains are independent, so while
+//               one pair evaluates sigma the tensor core works on the other tile's PV and S.
+//   warp 18     TMEM allocator; warp 19 padded-row fill of O
+// TMEM: S_A [0,128), S_B [128,256), O_A [256, 256+D), O_B [256+D, 256+2D).
+// Compared with fwd.cuh (one query tile, the two pairs alternating key tiles through a 3-deep S
+// ring), a pair's next S never waits for the other pair's P, which is what serialised sigma and
+// the MMAs there.
+#pragma once
+#include "fwd.cuh"
+
+namespace sigattn {
+
+template <int D>
+struct Fwd2Cfg {
+  static constexpr int kStages = (D == 64) ? 4 : 2;     // K / V ring
+  static constexpr int kQBufs = (D == 64) ? 2 : 1;      // Q-pair buffers
+  static constexpr int kSub = D / 64;
+  static constexpr int kTileBytes = kTile * D * 2;
+  static constexpr int kQOff = 0;                                   // Q[kQBufs][2 tiles]
+  static constexpr int kKOff = kQOff + kQBufs * 2 * kTileBytes;     // K[kStages]
+  static constexpr int kVOff = kKOff + kStages * kTileBytes;        // V[kStages]
+  static constexpr int kBarOff = kVOff + kStages * kTileBytes;
+  static constexpr int kNumBars = 2 * kQBufs + 4 * kStages + 2 + 2 + 2 + 2;
+  static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
+  static constexpr int kWarpTMA = 16, kWarpMMA = 17, kWarpAlloc = 18, kWarpFill = 19;
+  static constexpr int kThreads = 32 * 20;
+  static constexpr uint32_t kTmemCols = 512;
+  static constexpr uint32_t kColO = 256;                            // O_A, then O_B at kColO + D
+  static_assert(kColO + 2 * D <= kTmemCols, "TMEM budget");
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+};
+
+template <int D, bool kBf16, bool kOutF32>
+__global__ void __launch_bounds__(Fwd2Cfg<D>::kThreads, 1)
+sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
+  using C = Fwd2Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* q_full = bars;                     // [kQBufs]
+  uint64_t* q_empty = q_full + C::kQBufs;      // [kQBufs]
+  uint64_t* k_full = q_empty + C::kQBufs;      // [kStages]
+  uint64_t* v_full = k_full + C::kStages;
+  uint64_t* k_empty = v_full + C::kStages;     // K slot free: S of both tiles done
+  uint64_t* v_empty = k_empty + C::kStages;    // V slot free: PV of both tiles done
+  uint64_t* s_full = v_empty + C::kStages;     // [2] per query tile X
+  uint64_t* p_full = s_full + 2;               // [2]
+  uint64_t* o_full = p_full + 2;               // [2]
+  uint64_t* o_empty = o_full + 2;              // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+
+  const uint32_t warp = sm100::warp_id();
+  const uint32_t lane = sm100::lane_id();
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::kQBufs; ++i) {
+      sm100::mbar_init(&q_full[i], 1);
+      sm100::mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < C::kStages; ++i) {
+      sm100::mbar_init(&k_full[i], 1);
+      sm100::mbar_init(&v_full[i], 1);
+      sm100::mbar_init(&k_empty[i], 1);
+      sm100::mbar_init(&v_empty[i], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      sm100::mbar_init(&s_full[x], 1);
+      sm100::mbar_init(&p_full[x], 8);     // the 8 warps of pair x
+      sm100::mbar_init(&o_full[x], 1);
+      sm100::mbar_init(&o_empty[x], 8);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == C::kWarpTMA && lane == 0) {
+    sm100::tma_prefetch_desc(&tmQ);
+    sm100::tma_prefetch_desc(&tmK);
+    sm100::tma_prefetch_desc(&tmV);
+  }
+  if (warp == C::kWarpAlloc) sm100::tmem_alloc<C::kTmemCols>(tmem_holder);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int n_items = *args.n_items;
+  // tiles of this item that hold a valid query: A always, B when 2p + 1 < ceil(n_q / 128)
+  auto has_b = [&](int b, int pi) {
+    const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
+    return 2 * pi + 1 < (nq + kTile - 1) / kTile;
+  };
+
+  if (warp == C::kWarpTMA) {
+    // ===================== TMA producer =====================
+    const uint64_t pol_q = sm100::policy_evict_first();
+    const uint64_t pol_kv = sm100::policy_evict_last();
+    uint32_t kv_it = 0, c = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      const int b = item.x, h = item.y, pi = item.z, nkt = item.w;
+      if (nkt <= 0) continue;
+      const int zh = b * args.H + h;
+      const int ntq = has_b(b, pi) ? 2 : 1;
+      const uint32_t qb = c % C::kQBufs;
+      sm100::mbar_wait_backoff(&q_empty[qb], ((c / C::kQBufs) & 1) ^ 1);
+      if (sm100::elect_one()) {
+        sm100::mbar_arrive_expect_tx(&q_full[qb], ntq * C::kTileBytes);
+        for (int x = 0; x < ntq; ++x)
+#pragma unroll
+          for (int s = 0; s < C::kSub; ++s)
+            sm100::tma_load_3d(smem + C::kQOff + (qb * 2 + x) * C::kTileBytes + s * (kTile * 128), &tmQ, &q_full[qb],
+                               s * 64, (2 * pi + x) * kTile, zh, pol_q);
+      }
+      __syncwarp();
+      for (int j = 0; j < nkt; ++j, ++kv_it) {
+        const uint32_t st = kv_it % C::kStages, ph = (kv_it / C::kStages) & 1;
+        sm100::mbar_wait_backoff(&k_empty[st], ph ^ 1);
+        if (sm100::elect_one()) {
+          sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
+#pragma unroll
+          for (int s = 0; s < C::kSub; ++s)
+            sm100::tma_load_3d(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
+                               j * kTile, zh, pol_kv);
+        }
+        __syncwarp();
+        sm100::mbar_wait_backoff(&v_empty[st], ph ^ 1);
+        if (sm100::elect_one()) {
+          sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
+#pragma unroll
+          for (int s = 0; s < C::kSub; ++s)
+            sm100::tma_load_3d(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
+                               j * kTile, zh, pol_kv);
+        }
+        __syncwarp();
+      }
+      ++c;
+    }
+  } else if (warp == C::kWarpMMA) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 128, false, false);
+    constexpr uint32_t idesc_o = sm100::make_idesc_f16(kBf16, 128, D, false, true);
+    const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
+    const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
+    const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
+    uint32_t kv_it = 0, c = 0;
+    uint32_t xs[2] = {0, 0};   // S / P phase counter per query-tile slot
+    uint32_t xo[2] = {0, 0};   // O phase counter per slot
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      const int nkt = item.w;
+      if (nkt <= 0) continue;
+      const int ntq = has_b(item.x, item.z) ? 2 : 1;
+      const uint32_t qb = c % C::kQBufs;
+      sm100::mbar_wait(&q_full[qb], (c / C::kQBufs) & 1);
+      // S_x(j) = Q_x K_j^T into slot x's buffer; the last S of key tile j releases K_j
+      auto issue_s = [&](int x, int j) {
+        const uint32_t kvi = kv_it + j, st = kvi % C::kStages;
+        if (x == 0) sm100::mbar_wait(&k_full[st], (kvi / C::kStages) & 1);
+        sm100::tc_fence_after();
+        const uint32_t qa = q_base + (qb * 2 + x) * C::kTileBytes, ka = k_base + st * C::kTileBytes;
+        if (sm100::elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
+            sm100::mma_ss(tmem + x * 128, sm100::make_sdesc_sw128(qa + off, 16, 1024),
+                          sm100::make_sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
+          }
+          sm100::mma_commit(&s_full[x]);
+          if (x == ntq - 1) sm100::mma_commit(&k_empty[st]);
+        }
+        __syncwarp();
+      };
+      // O_x += P_x(j) V_j; the last PV of key tile j releases V_j
+      auto issue_pv = [&](int x, int j) {
+        const uint32_t kvi = kv_it + j, st = kvi % C::kStages;
+        sm100::mbar_wait_backoff(&p_full[x], xs[x] & 1);
+        if (j == 0) sm100::mbar_wait(&o_empty[x], (xo[x] & 1) ^ 1);   // epilogue drained O_x
+        if (x == 0) sm100::mbar_wait(&v_full[st], (kvi / C::kStages) & 1);
+        sm100::tc_fence_after();
+        const uint32_t va = v_base + st * C::kTileBytes;
+        if (sm100::elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < kTile / 16; ++kk) {
+            // P for keys [16kk, 16kk+16): warpgroup kk/4 packed its 64 keys at S cols [64 (kk/4), +32)
+            const uint32_t a_col = x * 128 + (kk >> 2) * 64 + (kk & 3) * 8;
+            sm100::mma_ts(tmem + C::kColO + x * D, tmem + a_col,
+                          sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
+                          (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          if (x == ntq - 1) sm100::mma_commit(&v_empty[st]);
+        }
+        __syncwarp();
+        ++xs[x];
+      };
+      for (int x = 0; x < ntq; ++x) issue_s(x, 0);
+      for (int j = 0; j < nkt; ++j)
+        for (int x = 0; x < ntq; ++x) {
+          issue_pv(x, j);                      // reads P_x(j) out of the S_x buffer ...
+          if (j + 1 < nkt) issue_s(x, j + 1);  // ... which S_x(j+1) then overwrites (in-order)
+        }
+      if (sm100::elect_one()) {
+        sm100::mma_commit(&q_empty[qb]);
+        for (int x = 0; x < ntq; ++x) sm100::mma_commit(&o_full[x]);
+      }
+      __syncwarp();
+      for (int x = 0; x < ntq; ++x) ++xo[x];
+      kv_it += nkt;
+      ++c;
+    }
+  } else if (warp < C::kWarpTMA) {
+    // ===================== sigma warps + epilogue, pair x = query tile slot =====================
+    const uint32_t x = warp >> 3;
+    const uint32_t gp = (warp >> 2) & 1;         // key columns [64 gp, +64) of the tile
+    const uint32_t quarter = warp & 3;
+    const uint32_t row = quarter * 32 + lane;
+    const uint32_t lane_addr = (quarter * 32) << 16;
+    uint32_t xs = 0, xo = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int4 item = args.items[it];
+      const int b = item.x, h = item.y, pi = item.z, nkt = item.w;
+      if (nkt <= 0) continue;
+      if (x == 1 && !has_b(b, pi)) continue;     // odd tile count: no second tile in this item
+      const int qt = 2 * pi + (int)x;
+      const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
+      const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
+      const float bias = args.bias_per_seq ? args.bias_per_seq[b] : args.bias;
+      const float a2 = args.scale * kLog2e;
+      const float b2 = bias * kLog2e;
+      const bool row_valid = qt * kTile + (int)row < nq;
+      for (int j = 0; j < nkt; ++j, ++xs) {
+        sm100::mbar_wait(&s_full[x], xs & 1);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const uint32_t col = x * 128 + gp * 64 + ch * 32;
+          const int nvalid = nk - (j * kTile + (int)gp * 64 + ch * 32);
+          float r[32];
+          uint32_t pk[16];
+          sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+          if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+          else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+          sm100::tmem_st16(tmem + lane_addr + x * 128 + gp * 64 + ch * 16, pk);
+        }
+        sm100::tmem_wait_st();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&p_full[x]);
+      }
+      // ---- epilogue: O_x rows, columns [gp D/2, +D/2) in 32-column pieces
+      sm100::mbar_wait(&o_full[x], xo & 1);
+      sm100::tc_fence_after();
+      const int qrow = qt * kTile + (int)row;
+      const bool valid = qrow < nq;
+      const size_t rowoff = ((size_t)(b * args.H + h) * args.Nq + qrow) * D;
+#pragma unroll
+      for (int pc = 0; pc < D / 64; ++pc) {
+        const int c0 = (int)gp * (D / 2) + pc * 32;
+        uint32_t ov[32];
+        sm100::tmem_ld32_sync(tmem + lane_addr + C::kColO + x * D + c0, ov);
+        if (pc == D / 64 - 1) {
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&o_empty[x]);
+        }
+        if (qrow < args.Nq) {
+          if constexpr (kOutF32) {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + rowoff + c0);
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              dst[e >> 2] = valid ? make_float4(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1]),
+                                                __uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3]))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + rowoff + c0);
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) {
+              uint4 w;
+              w.x = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 0]), __uint_as_float(ov[e + 1])) : 0u;
+              w.y = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3])) : 0u;
+              w.z = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 4]), __uint_as_float(ov[e + 5])) : 0u;
+              w.w = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 6]), __uint_as_float(ov[e + 7])) : 0u;
+              dst[e >> 3] = w;
+            }
+          }
+        }
+      }
+      ++xo;
+    }
+  }
+
+  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill && args.fill_pad)   // padded O rows beyond the last valid tile
+    pad_fill_warp(args.o, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
+                  kTile, lane);
+
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+}
+
+}  // namespace sigattn

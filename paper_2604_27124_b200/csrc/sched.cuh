@@ -23,6 +23,7 @@ __device__ __forceinline__ int clamp_len(const int32_t* lens, int b, int N) {
 
 // Work items: kind 0 (forward)  -> (b, h, q-tile) for q-tiles holding a valid query, cost = key tiles
 //             kind 1 (backward) -> (b, h, k-tile) for k-tiles holding a valid key,  cost = query tiles
+//             kind 2 (forward, two query tiles per item) -> (b, h, q-tile pair), cost = key tiles
 // Items with cost 0 are not emitted (their outputs are all padding and are zero-filled).
 // Order: sequences by cost descending (ties: b ascending); within a sequence h-major, tile-minor.
 // One CTA of kSchedThreads threads; B <= kMaxSchedB.  Shared memory: 4 B + 1 ints.
@@ -38,8 +39,8 @@ __device__ __forceinline__ void build_worklist_block(int kind, int B, int H, int
     const int nq = clamp_len(seqlens_q, b, Nq);
     const int nk = clamp_len(seqlens_k, b, Nk);
     const int tq = (nq + 127) / 128, tk = (nk + 127) / 128;
-    int c = kind == 0 ? tk : tq;
-    int t = kind == 0 ? tq : tk;
+    int c = kind == 1 ? tq : tk;
+    int t = kind == 0 ? tq : (kind == 1 ? tk : (tq + 1) / 2);   // kind 2: pairs of query tiles
     if (c == 0) t = 0;
     cost[b] = c;
     ntile[b] = t;
