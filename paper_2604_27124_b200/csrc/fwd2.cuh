@@ -31,12 +31,16 @@ struct Fwd2Cfg {
   static constexpr int kKOff = kQOff + kQBufs * 2 * kTileBytes;     // K[kStages]
   static constexpr int kVOff = kKOff + kStages * kTileBytes;        // V[kStages]
   static constexpr int kBarOff = kVOff + kStages * kTileBytes;
-  static constexpr int kNumBars = 2 * kQBufs + 4 * kStages + 2 + 2 + 2 + 2;
+  static constexpr int kNumBars = 2 * kQBufs + 4 * kStages + 2 + 2 + 2 + 2 + 2 + 2;
+  // d = 64: P gets its own TMEM columns so a pair releases S_x(j) once it has READ it (mid-sigma)
+  // and S_x(j+1) is computed while the pair still works on sigma(j); d = 128 has no room (P aliased).
+  static constexpr bool kSepP = (D == 64);
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kWarpTMA = 16, kWarpMMA = 17, kWarpAlloc = 18, kWarpFill = 19;
   static constexpr int kThreads = 32 * 20;
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr uint32_t kColO = 256;                            // O_A, then O_B at kColO + D
+  static constexpr uint32_t kColP = 256;                            // kSepP: P_A, P_B (64 cols each)
+  static constexpr uint32_t kColO = kSepP ? 384 : 256;              // O_A, then O_B at kColO + D
   static_assert(kColO + 2 * D <= kTmemCols, "TMEM budget");
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 };
@@ -59,6 +63,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
   uint64_t* p_full = s_full + 2;               // [2]
   uint64_t* o_full = p_full + 2;               // [2]
   uint64_t* o_empty = o_full + 2;              // [2]
+  uint64_t* s_free = o_empty + 2;              // [2] kSepP: pair x has read S_x(j)
+  uint64_t* pv_done = s_free + 2;              // [2] kSepP: PV_x(j) has read P_x(j)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -80,6 +86,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
       sm100::mbar_init(&p_full[x], 8);     // the 8 warps of pair x
       sm100::mbar_init(&o_full[x], 1);
       sm100::mbar_init(&o_empty[x], 8);
+      sm100::mbar_init(&s_free[x], 8);
+      sm100::mbar_init(&pv_done[x], 1);
     }
     sm100::fence_barrier_init();
   }
@@ -192,22 +200,36 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 #pragma unroll
           for (int kk = 0; kk < kTile / 16; ++kk) {
             // P for keys [16kk, 16kk+16): warpgroup kk/4 packed its 64 keys at S cols [64 (kk/4), +32)
-            const uint32_t a_col = x * 128 + (kk >> 2) * 64 + (kk & 3) * 8;
+            const uint32_t a_col = C::kSepP ? C::kColP + x * 64 + (kk >> 2) * 32 + (kk & 3) * 8
+                                            : x * 128 + (kk >> 2) * 64 + (kk & 3) * 8;
             sm100::mma_ts(tmem + C::kColO + x * D, tmem + a_col,
                           sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
                           (j > 0 || kk > 0) ? 1u : 0u);
           }
           if (x == ntq - 1) sm100::mma_commit(&v_empty[st]);
+          if (C::kSepP) sm100::mma_commit(&pv_done[x]);
         }
         __syncwarp();
         ++xs[x];
       };
       for (int x = 0; x < ntq; ++x) issue_s(x, 0);
-      for (int j = 0; j < nkt; ++j)
-        for (int x = 0; x < ntq; ++x) {
-          issue_pv(x, j);                      // reads P_x(j) out of the S_x buffer ...
-          if (j + 1 < nkt) issue_s(x, j + 1);  // ... which S_x(j+1) then overwrites (in-order)
+      if constexpr (C::kSepP) {
+        // events arrive as s_free_A(j), s_free_B(j), p_full_A(j), p_full_B(j): issue in that order
+        for (int j = 0; j < nkt; ++j) {
+          if (j + 1 < nkt)
+            for (int x = 0; x < ntq; ++x) {
+              sm100::mbar_wait(&s_free[x], xs[x] & 1);   // pair x has read S_x(j)
+              issue_s(x, j + 1);
+            }
+          for (int x = 0; x < ntq; ++x) issue_pv(x, j);
         }
+      } else {
+        for (int j = 0; j < nkt; ++j)
+          for (int x = 0; x < ntq; ++x) {
+            issue_pv(x, j);                      // reads P_x(j) out of the S_x buffer ...
+            if (j + 1 < nkt) issue_s(x, j + 1);  // ... which S_x(j+1) then overwrites (in-order)
+          }
+      }
       if (sm100::elect_one()) {
         sm100::mma_commit(&q_empty[qb]);
         for (int x = 0; x < ntq; ++x) sm100::mma_commit(&o_full[x]);
@@ -247,9 +269,22 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
           float r[32];
           uint32_t pk[16];
           sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+          if (C::kSepP && ch == 1) {   // all of this warp's S_x(j) columns are read: release the buffer
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&s_free[x]);
+          }
           if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
           else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
-          sm100::tmem_st16(tmem + lane_addr + x * 128 + gp * 64 + ch * 16, pk);
+          if (C::kSepP) {
+            if (ch == 0) {   // PV_x(j-1) has read the previous P_x
+              sm100::mbar_wait(&pv_done[x], (xs & 1) ^ 1);
+              sm100::tc_fence_after();
+            }
+            sm100::tmem_st16(tmem + lane_addr + C::kColP + x * 64 + gp * 32 + ch * 16, pk);
+          } else {
+            sm100::tmem_st16(tmem + lane_addr + x * 128 + gp * 64 + ch * 16, pk);
+          }
         }
         sm100::tmem_wait_st();
         sm100::tc_fence_before();
