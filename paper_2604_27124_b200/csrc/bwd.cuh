@@ -118,19 +118,18 @@ struct BwdCfg {
 };
 
 
-// Walks this CTA's non-empty work items (static stride) and their query tiles.
+// Walks this CTA's non-empty work items (first_item / next_item order) and their query tiles.
 struct TileIter {
-  int it, step, n_items, i, nqt;
+  int it, n_items, i, nqt;
   uint32_t item_c;   // index of the current item among this CTA's non-empty items
   bool valid;
   __device__ __forceinline__ void seek(const int4* items) {
-    while (it < n_items && items[it].w <= 0) it += step;
+    while (it < n_items && items[it].w <= 0) it = next_item(it);
     valid = it < n_items;
     nqt = valid ? items[it].w : 0;
   }
   __device__ __forceinline__ void init(const int4* items, int n) {
-    it = blockIdx.x;
-    step = gridDim.x;
+    it = first_item();
     n_items = n;
     i = 0;
     item_c = 0;
@@ -139,7 +138,7 @@ struct TileIter {
   __device__ __forceinline__ void advance(const int4* items) {
     if (++i >= nqt) {
       i = 0;
-      it += step;
+      it = next_item(it);
       ++item_c;
       seek(items);
     }
@@ -239,7 +238,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint64_t pol_kv = sm100::policy_evict_first();
     const uint64_t pol_q = sm100::policy_evict_last();
     uint32_t kv_c = 0, t = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
       if (nqt <= 0) continue;
@@ -449,7 +448,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
     uint32_t t = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, kt = item.z, nqt = item.w;
       if (nqt <= 0) continue;
@@ -566,7 +565,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     uint32_t t = 0, item_c = 0;
     bool pend = false;            // a dQ tile waiting to be drained
     int pend_zh = 0, pend_i = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
       if (nqt <= 0) continue;

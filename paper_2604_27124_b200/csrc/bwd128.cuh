@@ -108,7 +108,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     const uint64_t pol_kv = sm100::policy_evict_first();
     const uint64_t pol_q = sm100::policy_evict_last();
     uint32_t kv_c = 0, t = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       if (item.w <= 0) continue;
       const int b = item.x, h = item.y, kt = item.z, nqt = item_tiles(b);
@@ -177,7 +177,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 
     uint32_t t = 0, item_c = 0;
     bool primed = false;   // S/dP of the current tile already issued
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       if (item.w <= 0) continue;
       const int nqt = item_tiles(item.x);
@@ -243,7 +243,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     const uint32_t s_col = C::kColS + w4 * 16, dp_col = C::kColDP + w4 * 16;
     const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
     uint32_t t = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       if (item.w <= 0) continue;
       const int b = item.x, kt = item.z, nqt = item_tiles(b);
@@ -291,7 +291,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     const uint32_t lane_addr = (quarter * 32) << 16;
     const float alpha = args.scale;
     uint32_t t = 0, item_c = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       if (item.w <= 0) continue;
       const int b = item.x, h = item.y, kt = item.z, nqt = item_tiles(b);

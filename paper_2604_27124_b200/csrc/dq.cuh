@@ -120,7 +120,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     const uint64_t pol_q = sm100::policy_evict_first();
     const uint64_t pol_kv = sm100::policy_evict_last();
     uint32_t kv_it = 0, c = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, qt = item.z, nkt = item.w;
       if (nkt <= 0) continue;
@@ -170,7 +170,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
     const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
     uint32_t kv_it = 0, u_it = 0, c = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int nkt = args.items[it].w;
       if (nkt <= 0) continue;
       const uint32_t qb = c % C::kQBufs;
@@ -247,7 +247,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     const uint32_t row = quarter * 32 + lane;
     const uint32_t lane_addr = (quarter * 32) << 16;
     uint32_t u_it = 0, c = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, qt = item.z, nkt = item.w;
       if (nkt <= 0) continue;

@@ -153,7 +153,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint64_t pol_q = sm100::policy_evict_first();
     const uint64_t pol_kv = sm100::policy_evict_last();
     uint32_t kv_it = 0, c = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, qt = item.z, nkt = item.w;
       if (nkt <= 0) continue;
@@ -202,7 +202,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
     const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
     uint32_t kv_it = 0, s_it = 0, c = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int nkt = args.items[it].w;
       if (nkt <= 0) continue;
       const uint32_t qb = c & 1;
@@ -276,7 +276,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t row = quarter * 32 + lane;    // tile row = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
     uint32_t s_it = 0, c = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, qt = item.z, nkt = item.w;
       if (nkt <= 0) continue;

@@ -113,7 +113,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     const uint64_t pol_q = sm100::policy_evict_first();
     const uint64_t pol_kv = sm100::policy_evict_last();
     uint32_t kv_it = 0, c = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, pi = item.z, nkt = item.w;
       if (nkt <= 0) continue;
@@ -163,7 +163,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     uint32_t kv_it = 0, c = 0;
     uint32_t xs[2] = {0, 0};   // S / P phase counter per query-tile slot
     uint32_t xo[2] = {0, 0};   // O phase counter per slot
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int nkt = item.w;
       if (nkt <= 0) continue;
@@ -247,7 +247,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     const uint32_t row = quarter * 32 + lane;
     const uint32_t lane_addr = (quarter * 32) << 16;
     uint32_t xs = 0, xo = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, pi = item.z, nkt = item.w;
       if (nkt <= 0) continue;
