@@ -49,6 +49,7 @@ def _load():
         lib.sigattn_oracle_dq_rows.argtypes = [i, i, i, i, _D, _D, _D, _D, _I, _I, dd, _D, i, i, _I, i, _D]
         lib.sigattn_oracle_dkdv_rows.argtypes = [i, i, i, i, _D, _D, _D, _D, _I, _I, dd, _D, i, i, _I, i, _D, _D]
         lib.sigattn_oracle_p_ds.argtypes = [i, i, i, i, _D, _D, _D, _D, _I, _I, dd, _D, i, i, _D, _D, _D]
+        lib.sigattn_oracle_dbias.argtypes = [i, i, i, i, i, _D, _D, _D, _D, _I, _I, dd, _D, _D]
         lib.sigattn_oracle_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -103,6 +104,17 @@ def bwd(q, k, v, dout, nq=None, nk=None, alpha=None, bias=None):
     _load().sigattn_oracle_bwd(B, H, Nq, Nk, d, _p(q), _p(k), _p(v), _p(dout), _p(nq), _p(nk), alpha,
                                _p(bias), _p(dq), _p(dk), _p(dv))
     return dq, dk, dv
+
+
+def dbias(q, k, v, dout, nq=None, nk=None, alpha=None, bias=None) -> np.ndarray:
+    """d sum(dout * O) / d b_z for the per-sequence bias: sum over heads and valid (i, j) of dS; [B]."""
+    q, k, v, nq, nk, bias, (B, H, Nq, Nk, d) = _prep(q, k, v, nq, nk, bias)
+    dout = _f64(dout)
+    alpha = 1.0 / np.sqrt(d) if alpha is None else float(alpha)
+    db = np.zeros((B,), np.float64)
+    _load().sigattn_oracle_dbias(B, H, Nq, Nk, d, _p(q), _p(k), _p(v), _p(dout), _p(nq), _p(nk), alpha,
+                                 _p(bias), _p(db))
+    return db
 
 
 def fwd_rows(q, k, v, b, h, rows, nq=None, nk=None, alpha=None, bias=None) -> np.ndarray:

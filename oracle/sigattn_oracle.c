@@ -18,6 +18,7 @@
  *   dQ_i  = alpha * sum_j dS_ij k_j                                Alg. 2
  *   dK_j  = alpha * sum_i dS_ij q_i                                Alg. 3
  *   padded rows of dQ, dK, dV are 0                                Alg. 2, Alg. 3
+ *   db_z  = sum_h sum_(i,j valid) dS_ij   (learnable bias)  x_ij = ... + b_z, chain rule
  *
  * Mask reading (reading R2): "S + (-inf)(1 - mask)" is read as a select,
  * sigma(-inf) := 0 exactly; no -inf arithmetic is performed.
@@ -218,6 +219,32 @@ void sigattn_oracle_p_ds(int H, int Nq, int Nk, int d, const double* q, const do
             dP[e] = dp;
             dS[e] = p * (1.0 - p) * dp;
         }
+}
+
+/* Gradient of sum(dout * O) w.r.t. the per-sequence bias b_z ("fixed or learnable"; x =
+ * alpha s + b_z enters every valid logit of sequence z, so dL/db_z = sum over heads h and valid
+ * (i, j) of dS_ij, dS = P (1 - P) dP as in Alg. 2 line P:663).  db is [B]. */
+void sigattn_oracle_dbias(int B, int H, int Nq, int Nk, int d, const double* q, const double* k,
+                          const double* v, const double* dout, const int32_t* nq, const int32_t* nk,
+                          double alpha, const double* bias, double* db) {
+    for (int b = 0; b < B; ++b) {
+        int nqb = clampn(nq[b], Nq), nkb = clampn(nk[b], Nk);
+        double acc = 0.0;
+#pragma omp parallel for reduction(+ : acc) schedule(dynamic, 4)
+        for (long long r = 0; r < (long long)H * nqb; ++r) {
+            int h = (int)(r / (nqb > 0 ? nqb : 1)), i = (int)(r % (nqb > 0 ? nqb : 1));
+            const double* qs = q + slice(b, h, H, Nq, d);
+            const double* ks = k + slice(b, h, H, Nk, d);
+            const double* vs = v + slice(b, h, H, Nk, d);
+            const double* dos = dout + slice(b, h, H, Nq, d);
+            for (int j = 0; j < nkb; ++j) {
+                double p = p_entry(qs, ks, d, nqb, nkb, alpha, bias[b], i, j);
+                double dp = dot(dos + (size_t)i * d, vs + (size_t)j * d, d);
+                acc += p * (1.0 - p) * dp;
+            }
+        }
+        db[b] = acc;
+    }
 }
 
 int sigattn_oracle_threads(void) {

@@ -275,3 +275,46 @@ def test_alpha_enters_dq_dk_once():
     np.testing.assert_allclose(dq2, 2 * dq1, rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(dk2, dk1, rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(dv2, dv1, rtol=1e-12, atol=1e-15)
+
+
+# --------------------------------------------------------------------------------------------
+# learnable per-sequence bias ("fixed or learnable"): d L / d b_z
+@pytest.mark.parametrize("case", [dict(), dict(Nq=7, Nk=11, nq=[5, 0], nk=[11, 4])])
+def test_dbias_against_torch_autograd(case):
+    """oracle.dbias == torch fp64 autograd of Eq. 2 w.r.t. a per-sequence bias tensor (<= 1e-12)."""
+    q, k, v, do, nq, nk = rand_case(seed=11, **case)
+    alpha = 0.45
+    bias = np.array([-0.7 + 0.4 * b for b in range(q.shape[0])])
+    B, H, Nq, d = q.shape
+    Nk = k.shape[2]
+    bt = torch.tensor(bias, requires_grad=True)
+    mq = torch.arange(Nq)[None, :] < torch.tensor(nq)[:, None]
+    mk = torch.arange(Nk)[None, :] < torch.tensor(nk)[:, None]
+    valid = (mq[:, :, None] & mk[:, None, :])[:, None]
+    s = alpha * torch.matmul(torch.tensor(q), torch.tensor(k).transpose(-1, -2)) + bt[:, None, None, None]
+    p = torch.where(valid, torch.sigmoid(s), torch.zeros((), dtype=torch.float64))
+    o = torch.where(mq[:, None, :, None], torch.matmul(p, torch.tensor(v)), torch.zeros((), dtype=torch.float64))
+    (o * torch.tensor(do)).sum().backward()
+    got = oracle.dbias(q, k, v, do, nq, nk, alpha, bias)
+    ref = bt.grad.numpy()
+    assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+def test_dbias_finite_differences_and_invariants():
+    """Central FD of L(b) (h=1e-5, rel <= 1e-7); db is 0 for a sequence with no valid key;
+    db is linear in dO and equals the sum over heads of the per-head dS sums (oracle.p_ds)."""
+    q, k, v, do, nq, nk = rand_case(B=3, H=2, Nq=5, d=3, nq=[5, 3, 2], nk=[5, 0, 4], seed=12)
+    alpha, bias = 0.6, np.array([-0.2, -1.0, 0.3])
+    db = oracle.dbias(q, k, v, do, nq, nk, alpha, bias)
+    h = 1e-5
+    for b in range(3):
+        bp, bm = bias.copy(), bias.copy()
+        bp[b] += h
+        bm[b] -= h
+        fd = ((oracle.fwd(q, k, v, nq, nk, alpha, bp) - oracle.fwd(q, k, v, nq, nk, alpha, bm)) * do).sum() / (2 * h)
+        assert abs(db[b] - fd) <= 1e-7 * max(1.0, abs(fd))
+    assert db[1] == 0.0
+    assert np.allclose(oracle.dbias(q, k, v, 2.5 * do, nq, nk, alpha, bias), 2.5 * db, rtol=1e-12, atol=0)
+    for b in range(3):
+        tot = sum(oracle.p_ds(q, k, v, do, b, hh, nq, nk, alpha, bias)[2].sum() for hh in range(2))
+        assert abs(tot - db[b]) <= 1e-12 * max(1.0, abs(tot))
