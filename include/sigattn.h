@@ -70,6 +70,10 @@ typedef struct {
   float bias;        /* scalar b, used when bias_per_seq == NULL (b = -log n)     */
   const float* bias_per_seq; /* device [B] or NULL: per-sequence b in R^Z (Alg. 1)  */
   unsigned flags;    /* SIGATTN_F_*                                                      */
+  float* dbias;      /* sigattn_bwd only: device [B] fp32 or NULL.  When set, receives
+                        d loss / d b_z = sum over heads and valid (i, j) of dS_ij (the gradient
+                        of a learnable per-sequence bias); overwritten, not accumulated.
+                        Summed with fp32 atomics: not bitwise reproducible run to run.      */
 } sigattn_params;
 
 /* Forward (Alg. 1).  q [B,H,Nq,d], k/v [B,H,Nk,d], o [B,H,Nq,d] (fp32 if OUT_F32_PARTIAL).

@@ -34,6 +34,7 @@ class SigattnParams(ctypes.Structure):
         ("seqlens_q", ctypes.c_void_p), ("seqlens_k", ctypes.c_void_p),
         ("scale", ctypes.c_float), ("bias", ctypes.c_float),
         ("bias_per_seq", ctypes.c_void_p), ("flags", ctypes.c_uint),
+        ("dbias", ctypes.c_void_p),
     ]
 
 
@@ -87,6 +88,8 @@ def check(status: int):
         raise SigattnError(status, load().sigattn_last_error().decode())
 
 
-def make_params(B, H, Nq, Nk, d, dtype_code, seqlens_q_ptr, seqlens_k_ptr, scale, bias, bias_ptr, flags):
+def make_params(B, H, Nq, Nk, d, dtype_code, seqlens_q_ptr, seqlens_k_ptr, scale, bias, bias_ptr, flags,
+                dbias_ptr=None):
     return SigattnParams(int(B), int(H), int(Nq), int(Nk), int(d), int(dtype_code), seqlens_q_ptr or None,
-                         seqlens_k_ptr or None, float(scale), float(bias), bias_ptr or None, int(flags))
+                         seqlens_k_ptr or None, float(scale), float(bias), bias_ptr or None, int(flags),
+                         dbias_ptr or None)

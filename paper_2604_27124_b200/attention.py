@@ -112,11 +112,13 @@ def bwd_workspace_bytes(B, H, Nq, Nk, d, dtype=torch.bfloat16) -> int:
 
 def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias: BiasArg = None,
                 dq=None, dk=None, dv=None, workspace: Optional[torch.Tensor] = None, dq_f32: bool = False,
-                deterministic: bool = False):
+                deterministic: bool = False, dbias: Optional[torch.Tensor] = None):
     """Backward (Alg. 2 + Alg. 3, fused).  Returns (dQ, dK, dV); dQ is fp32 if dq_f32 (CP partial).
 
     deterministic=True runs the paper's two passes instead (dK/dV key-tile-owned, dQ
     query-tile-owned): no atomics, bitwise reproducible, ~40% more tensor work.
+    dbias: optional fp32 [B] CUDA tensor that receives dL/db_z = sum over heads and valid (i, j) of
+    dS_ij -- the gradient of a learnable per-sequence bias.
     """
     lib = _lib.load()
     B, H, Nq, Nk, d = _check_qkv(q, k, v)
@@ -130,7 +132,11 @@ def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias:
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
     flags = (_lib.SIGATTN_F_DQ_F32_PARTIAL if dq_f32 else 0) | (_lib.SIGATTN_F_BWD_DETERMINISTIC if deterministic else 0)
-    p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags)
+    if dbias is not None and (dbias.dtype != torch.float32 or dbias.numel() != B or not dbias.is_contiguous()
+                              or not dbias.is_cuda):
+        raise ValueError("sigattn: dbias must be a contiguous fp32 CUDA tensor with B entries")
+    p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags,
+                         _ptr(dbias))
     need = int(lib.sigattn_bwd_workspace_bytes(ctypes.byref(p)))
     if workspace is None or workspace.numel() * workspace.element_size() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
@@ -189,15 +195,19 @@ class SigmoidAttentionFn(torch.autograd.Function):
         ctx.scale = scale
         ctx.bias = None if isinstance(bias, torch.Tensor) else bias
         ctx.deterministic = deterministic
+        # a [B] bias tensor that requires grad is a learnable per-sequence bias
+        ctx.bias_grad = isinstance(bias, torch.Tensor) and bias.requires_grad and bias.numel() == q.shape[0]
         return o
 
     @staticmethod
     def backward(ctx, do):
         q, k, v, sq, sk, bt = ctx.saved_tensors
         bias = bt if bt is not None else ctx.bias
+        db = torch.empty(q.shape[0], dtype=torch.float32, device=q.device) if ctx.bias_grad else None
         dq, dk, dv = sigattn_bwd(q, k, v, do.contiguous(), sq, sk, ctx.scale, bias,
-                                 deterministic=ctx.deterministic)
-        return dq, dk, dv, None, None, None, None, None
+                                 deterministic=ctx.deterministic, dbias=db)
+        dbias = db.to(bt.dtype).reshape(bt.shape) if db is not None else None
+        return dq, dk, dv, None, None, None, dbias, None
 
 
 def sigmoid_attention(q, k, v, seqlens_q=None, seqlens_k=None, key_padding_mask=None,

@@ -89,6 +89,7 @@ struct BwdArgs {
   void* dk;               // [B,H,Nk,D]
   void* dv;
   void* dq_pad;           // 16-bit dQ output whose rows >= ceil128(n_q) the fill warp zeroes, or nullptr
+  float* dbias;           // [B] fp32, zeroed at entry, += sum of dS (learnable bias gradient); or nullptr
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots (8 events x 512 tiles)
 };
 
@@ -147,10 +148,12 @@ struct TileIter {
 
 // 16 query columns of one key row: P^T and dS^T = P^T (1 - P^T) dP^T, packed to 16 bits.
 // kMask: columns e >= nvalid (padded queries) give P = dS = 0 (nvalid = 0 for a padded key row).
-template <bool kMask, bool kBf16>
+// kSum: also accumulate the fp32 dS values into *dsum (learnable-bias gradient).
+template <bool kMask, bool kBf16, bool kSum = false>
 __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
-                                          float a2, float b2, bool key_valid, int nvalid) {
+                                          float a2, float b2, bool key_valid, int nvalid, float* dsum = nullptr) {
   sigma_row<16, kMask, SIGATTN_BWD_EMU>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
+  float s0 = 0.f, s1 = 0.f;
 #pragma unroll
   for (int e = 0; e < 16; e += 2) {
     float p0 = v[e], p1 = v[e + 1], u0, u1, d0, d1;
@@ -162,14 +165,23 @@ __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16],
       p1 = (e + 1 < nvalid) ? p1 : 0.0f;
       d1 = (e + 1 < nvalid) ? d1 : 0.0f;
     }
+    if constexpr (kSum) fadd2(s0, s1, s0, s1, d0, d1);
     pp[e >> 1] = sm100::pack2<kBf16>(p0, p1);
     dd[e >> 1] = sm100::pack2<kBf16>(d0, d1);
   }
+  if constexpr (kSum) *dsum += s0 + s1;
+}
+
+// Adds a warp's per-lane partial sums of dS into dbias[b] (one atomic per warp).
+__device__ __forceinline__ void dbias_flush(float* dbias, int b, float acc, uint32_t lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0 && acc != 0.0f) atomicAdd(dbias + b, acc);
 }
 
 // kDQ = false: dK, dV only (the key-tile-owned pass of the deterministic backward, Alg. 3;
 // dQ then comes from sigattn_dq_kernel, Alg. 2): no dQ MMA, no dS staging, no dQ reduction.
-template <int D, bool kBf16, bool kDQ = true>
+template <int D, bool kBf16, bool kDQ = true, bool kDB = false>
 __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
 sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -459,6 +471,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const float b2 = bias * kLog2e;
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
+      float db_acc = 0.f;
       for (int i = 0; i < nqt; ++i, ++t) {
 #pragma unroll
         for (int qh = 0; qh < 2; ++qh) {
@@ -483,8 +496,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           // rows of padded keys)
           const int ncol = nq - (i * kTile + qh * 64 + (int)w4 * 16);
           uint32_t pp[8], dd[8];
-          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16);
-          else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
+          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, &db_acc);
+          else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, &db_acc);
           BWD_TR(qh == 0 ? 1 : 4);
           // P^T / dS^T over the first half of this warp's own (already read) columns; the epilogue
           // warpgroup stages dS^T into shared memory for the dQ MMA
@@ -498,6 +511,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #undef BWD_TR
         }
       }
+      if constexpr (kDB) dbias_flush(args.dbias, b, db_acc, lane);
     }
   } else if (warp < C::kWarpTMA && !SIGATTN_DBG_MMAONLY && warp >= kComputeWarps) {
     // ===================== epilogue warpgroup: dS^T staging, dQ drain, dK/dV =====================

@@ -43,7 +43,7 @@ struct Bwd128Cfg {
 };
 
 // kDQ = false: dK, dV only (deterministic backward, Alg. 3); see bwd.cuh.
-template <bool kBf16, bool kDQ = true>
+template <bool kBf16, bool kDQ = true, bool kDB = false>
 __global__ void __launch_bounds__(Bwd128Cfg::kThreads, 1)
 sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -254,6 +254,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       const float b2 = bias * kLog2e;
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
+      float db_acc = 0.f;
       for (int i = 0; i < nqt; ++i, ++t) {
         sm100::mbar_wait(s_full, t & 1);
         if (kDQ) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
@@ -265,8 +266,8 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sm100::tmem_wait_ld_dep16(dp);
         const int ncol = nq - (i * C::kQT + (int)w4 * 16);
         uint32_t pp[8], dd[8];
-        if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16);
-        else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0);
+        if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, &db_acc);
+        else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, &db_acc);
         sm100::tmem_st8(tmem + lane_addr + s_col, pp);
         sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
         if constexpr (kDQ) {
@@ -283,6 +284,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(p_full);
       }
+      if constexpr (kDB) dbias_flush(args.dbias, b, db_acc, lane);
     }
   } else if (warp < C::kWarpTMA) {
     // ===================== epilogue: dQ^T drain (lane = d index) + dK/dV =====================

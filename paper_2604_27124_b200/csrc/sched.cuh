@@ -103,9 +103,11 @@ build_worklist_kernel(int kind, int B, int H, int Nq, int Nk, const int32_t* __r
 __global__ void __launch_bounds__(kSchedThreads)
 bwd_prep_kernel(int B, int H, int Nq, int Nk, int D, const int32_t* __restrict__ seqlens_q,
                 const int32_t* __restrict__ seqlens_k, int4* __restrict__ items, int* __restrict__ n_items,
-                float* __restrict__ dq_acc) {
+                float* __restrict__ dq_acc, float* __restrict__ dbias) {
   extern __shared__ int sh[];
   if (blockIdx.x == 0) {
+    if (dbias)
+      for (int i = threadIdx.x; i < B; i += blockDim.x) dbias[i] = 0.f;
     build_worklist_block(1, B, H, Nq, Nk, seqlens_q, seqlens_k, items, n_items, sh);
     return;
   }

@@ -137,6 +137,7 @@ sigattn_status launch_worklist(int kind, const sigattn_params* p, int4* items, i
 }
 
 sigattn_status launch_bwd_prep(const sigattn_params* p, int4* items, int* n_items, float* dq_acc, cudaStream_t s) {
+  // (also zeroes p->dbias when the bias gradient is requested)
   const int smem = sched_smem(p);
   if (smem > 48 * 1024) {
     sigattn_status st = set_smem(bwd_prep_kernel, (4 * kMaxSchedB + 1) * (int)sizeof(int));
@@ -144,7 +145,7 @@ sigattn_status launch_bwd_prep(const sigattn_params* p, int4* items, int* n_item
   }
   const int zero_ctas = dq_acc ? num_sms() : 0;
   bwd_prep_kernel<<<1 + zero_ctas, kSchedThreads, smem, s>>>(p->B, p->H, p->Nq, p->Nk, p->d, p->seqlens_q,
-                                                              p->seqlens_k, items, n_items, dq_acc);
+                                                              p->seqlens_k, items, n_items, dq_acc, p->dbias);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
@@ -195,8 +196,8 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   return SIGATTN_OK;
 }
 
-template <int D, bool kBf16, bool kDQ = true>
-sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
+template <int D, bool kBf16, bool kDQ = true, bool kDB = false>
+sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                           float* dq_acc, void* dk, void* dv,
                           const int4* items, const int* n_items, int max_items, cudaStream_t s,
                           void* dq_pad = nullptr) {
@@ -228,9 +229,10 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   a.dk = dk;
   a.dv = dv;
   a.dq_pad = dq_pad;
+  a.dbias = p->dbias;
   a.trace = g_trace;
   using C = BwdCfg<D>;
-  auto kern = sigattn_bwd_kernel<D, kBf16, kDQ>;
+  auto kern = sigattn_bwd_kernel<D, kBf16, kDQ, kDB>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);
@@ -241,8 +243,8 @@ sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k,
   return SIGATTN_OK;
 }
 
-template <bool kBf16, bool kDQ = true>
-sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
+template <bool kBf16, bool kDQ = true, bool kDB = false>
+sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                              float* dq_acc, void* dk, void* dv,
                              const int4* items, const int* n_items, int max_items, cudaStream_t s,
                              void* dq_pad = nullptr) {
@@ -270,8 +272,9 @@ sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void*
   a.dk = dk;
   a.dv = dv;
   a.dq_pad = dq_pad;
+  a.dbias = p->dbias;
   a.trace = g_trace;
-  auto kern = sigattn_bwd128_kernel<kBf16, kDQ>;
+  auto kern = sigattn_bwd128_kernel<kBf16, kDQ, kDB>;
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);
@@ -280,6 +283,22 @@ sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void*
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
+}
+
+// runtime dispatch of the bias-gradient variant (kDB: the compute warps also sum dS)
+template <int D, bool kBf16, bool kDQ = true>
+sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
+                          float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
+                          cudaStream_t s, void* dq_pad = nullptr) {
+  return p->dbias ? launch_bwd_t<D, kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad)
+                  : launch_bwd_t<D, kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad);
+}
+template <bool kBf16, bool kDQ = true>
+sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
+                             float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
+                             cudaStream_t s, void* dq_pad = nullptr) {
+  return p->dbias ? launch_bwd128_t<kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad)
+                  : launch_bwd128_t<kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad);
 }
 
 template <int D, bool kBf16, bool kF32>

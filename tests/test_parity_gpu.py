@@ -342,3 +342,41 @@ def test_deterministic_autograd():
         grads.append((qq.grad, kk.grad, vv.grad))
     assert torch.equal(grads[0][1], grads[1][1]) and torch.equal(grads[0][2], grads[1][2])
     assert relerr(f64(grads[1][0]), f64(grads[0][0])) < 1e-2
+
+
+# ---------------------------------------------------------------------------------------------
+# learnable per-sequence bias: dL/db_z = sum over heads and valid (i, j) of dS
+@pytest.mark.parametrize("cfg,det", [
+    (I.C1, False),
+    (I.Config("db_ragged", B=5, H=3, N=300, d=64, lengths=[300, 1, 129, 0, 256], seed=40), False),
+    (I.Config("db_ragged_det", B=5, H=3, N=300, d=64, lengths=[300, 1, 129, 0, 256], seed=40), True),
+    (I.Config("db_d128", B=3, H=2, N=260, d=128, lengths=[260, 65, 200], seed=41), False),
+    (I.Config("db_d128_det", B=3, H=2, N=260, d=128, lengths=[260, 65, 200], seed=41), True),
+])
+def test_bias_gradient(cfg, det):
+    sa = _sa()
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    bias = torch.tensor([-math.log(max(n, 1)) + 0.1 * i for i, n in enumerate(cfg.nk)], dtype=torch.float32,
+                        device="cuda")
+    db = torch.full((cfg.B,), float("nan"), dtype=torch.float32, device="cuda")   # must be overwritten
+    dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, bias=bias, dbias=db, deterministic=det)
+    torch.cuda.synchronize()
+    ref = oracle.dbias(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, 1.0 / math.sqrt(cfg.d),
+                       bias.double().cpu().numpy())
+    got = db.double().cpu().numpy()
+    # dS is summed in fp32 from the same sigma the kernel uses; the oracle is fp64 on the rounded inputs
+    assert np.abs(got - ref).max() <= 1e-2 * max(np.abs(ref).max(), 1e-6), (got, ref)
+    # the requested gradient does not change dQ, dK, dV
+    dq2, dk2, dv2 = sa.sigattn_bwd(q, k, v, do, nq, nk, bias=bias, deterministic=det)
+    assert torch.equal(dk, dk2) and torch.equal(dv, dv2)
+
+
+def test_bias_gradient_autograd():
+    sa = _sa()
+    cfg = I.Config("db_ag", B=3, H=2, N=256, d=64, lengths=[256, 100, 17], seed=42)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    bias = torch.tensor([-5.0, -4.0, -3.0], device="cuda", requires_grad=True)
+    o = sa.sigmoid_attention(q, k, v, seqlens_q=nq, seqlens_k=nk, bias=bias)
+    o.backward(do)
+    ref = oracle.dbias(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, 1 / 8, [-5.0, -4.0, -3.0])
+    assert np.abs(bias.grad.double().cpu().numpy() - ref).max() <= 1e-2 * np.abs(ref).max()
