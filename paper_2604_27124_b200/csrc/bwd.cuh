@@ -58,6 +58,9 @@
 #ifndef SIGATTN_DBG_NOSTAGE
 #define SIGATTN_DBG_NOSTAGE 0     // timing experiments only (wrong results): epilogue skips the dS smem staging
 #endif
+#ifndef SIGATTN_BWD_SPEC
+#define SIGATTN_BWD_SPEC 1        // tier-4 sigma evaluated before the warp vote (sigma_row_spec4)
+#endif
 #ifndef SIGATTN_BWD_EMU
 #define SIGATTN_BWD_EMU 0         // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
 #endif
@@ -149,10 +152,23 @@ struct TileIter {
 // 16 query columns of one key row: P^T and dS^T = P^T (1 - P^T) dP^T, packed to 16 bits.
 // kMask: columns e >= nvalid (padded queries) give P = dS = 0 (nvalid = 0 for a padded key row).
 // kSum: also accumulate the fp32 dS values into *dsum (learnable-bias gradient).
+// s_taddr: TMEM address the 16 scores were loaded from (still intact: each warp packs P / dS over its
+// own columns only after this call).  SIGATTN_BWD_SPEC: the tier-4 sigma is evaluated before the warp
+// vote; on a failed vote the scores are reloaded from s_taddr and the exact tiers run.
 template <bool kMask, bool kBf16, bool kSum = false>
 __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
-                                          float a2, float b2, bool key_valid, int nvalid, float* dsum = nullptr) {
+                                          float a2, float b2, bool key_valid, int nvalid, uint32_t s_taddr,
+                                          float* dsum = nullptr) {
+#if SIGATTN_BWD_SPEC
+  if (!sigma_row_spec4<16, kMask>(v, a2, b2, key_valid, nvalid)) {   // v: scores in, P out
+    sm100::tmem_ld16(s_taddr, v);
+    sm100::tmem_wait_ld_dep16(v);
+    sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid);
+  }
+#else
+  (void)s_taddr;
   sigma_row<16, kMask, SIGATTN_BWD_EMU>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
+#endif
   float s0 = 0.f, s1 = 0.f;
 #pragma unroll
   for (int e = 0; e < 16; e += 2) {
@@ -496,8 +512,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           // rows of padded keys)
           const int ncol = nq - (i * kTile + qh * 64 + (int)w4 * 16);
           uint32_t pp[8], dd[8];
-          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, &db_acc);
-          else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, &db_acc);
+          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, &db_acc);
+          else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, &db_acc);
           BWD_TR(qh == 0 ? 1 : 4);
           // P^T / dS^T over the first half of this warp's own (already read) columns; the epilogue
           // warpgroup stages dS^T into shared memory for the dQ MMA

@@ -266,8 +266,8 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sm100::tmem_wait_ld_dep16(dp);
         const int ncol = nq - (i * C::kQT + (int)w4 * 16);
         uint32_t pp[8], dd[8];
-        if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, &db_acc);
-        else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, &db_acc);
+        if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, &db_acc);
+        else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, &db_acc);
         sm100::tmem_st8(tmem + lane_addr + s_col, pp);
         sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
         if constexpr (kDQ) {

@@ -24,6 +24,9 @@
 #ifndef SIGATTN_DBG_FWD_NOSIGMA
 #define SIGATTN_DBG_FWD_NOSIGMA 0
 #endif
+#ifndef SIGATTN_FWD_SPEC
+#define SIGATTN_FWD_SPEC 1  // tier-4 sigma evaluated before the warp vote (sigma_row_spec4)
+#endif
 #ifndef SIGATTN_FWD_EMU
 #define SIGATTN_FWD_EMU 0   // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
 #endif
@@ -88,6 +91,33 @@ __device__ __forceinline__ void sigmoid_row32(float (&v)[32], uint32_t (&pk)[16]
     }
     pk[e >> 1] = sm100::pack2<kBf16>(p0, p1);
   }
+}
+
+// sigmoid_row32 for a chunk loaded from TMEM address taddr.  SIGATTN_FWD_SPEC: the tier-4 sigma is
+// evaluated speculatively before the warp vote; on a failed vote (some valid logit > -4, rare with
+// b = -log n) the scores are reloaded -- the chunk's S columns are not yet overwritten by P -- and
+// the exact tiers of sigma_row run.
+template <bool kMask, bool kBf16>
+__device__ __forceinline__ void sigmoid_chunk32(uint32_t taddr, float (&v)[32], uint32_t (&pk)[16], float a, float c,
+                                                bool row_valid, int nvalid) {
+#if SIGATTN_FWD_SPEC
+  if (!sigma_row_spec4<32, kMask>(v, a, c, row_valid, nvalid)) {
+    sm100::tmem_ld32_sync(taddr, v);
+    sigma_row<32, kMask, 0>(v, a, c, row_valid, nvalid);
+  }
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    float p0 = v[e], p1 = v[e + 1];
+    if constexpr (kMask) {
+      p0 = (e < nvalid) ? p0 : 0.0f;
+      p1 = (e + 1 < nvalid) ? p1 : 0.0f;
+    }
+    pk[e >> 1] = sm100::pack2<kBf16>(p0, p1);
+  }
+#else
+  (void)taddr;
+  sigmoid_row32<kMask, kBf16>(v, pk, a, c, row_valid, nvalid);
+#endif
 }
 
 template <int D, bool kBf16, bool kOutF32>
@@ -303,8 +333,8 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
           for (int e = 0; e < 16; ++e) pk[e] = __float_as_uint(r[2 * e]) ^ __float_as_uint(r[2 * e + 1]);
 #else
-          if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
-          else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+          if (nvalid >= 32) sigmoid_chunk32<false, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid);
+          else sigmoid_chunk32<true, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid);
 #endif
           // P over the first half of this warpgroup's 64 columns (chunk 0's columns are already read)
           sm100::tmem_st16(tmem + lane_addr + (si % C::kSBuf) * 128 + gp * 64 + ch * 16, pk);

@@ -274,8 +274,13 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&s_free[x]);
           }
-          if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
-          else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+          if (C::kSepP) {   // S already released: no reload possible, vote-first tiers
+            if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+            else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+          } else {
+            if (nvalid >= 32) sigmoid_chunk32<false, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid);
+            else sigmoid_chunk32<true, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid);
+          }
           if (C::kSepP) {
             if (ch == 0) {   // PV_x(j-1) has read the previous P_x
               sm100::mbar_wait(&pv_done[x], (xs & 1) ^ 1);

@@ -156,6 +156,34 @@ __device__ __forceinline__ void sigma2_from_t(float t0, float t1, float& p0, flo
   p1 = r1;
 }
 
+// Speculative form of the common case: N scores of one row -> N values of the <= -4 tier (in place),
+// evaluated BEFORE the warp vote, so the max/vote chain runs beside the MUFU work instead of in front
+// of it.  Returns the vote: true iff every valid logit of the warp's chunk is <= -4, i.e. the values
+// are the tier-4 sigma.  On false the caller must redo the chunk from its scores with sigma_row
+// (the scores are gone: callers reload them from TMEM, where they are still intact).  The vote looks
+// only at valid elements, as in sigma_row, so the choice never depends on pad content.
+template <int N, bool kMask = false>
+__device__ __forceinline__ bool sigma_row_spec4(float (&v)[N], float a, float c, bool lane_valid = true,
+                                                int nvalid = N) {
+  float m = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < N; e += 2) {
+    ffma2(v[e], v[e + 1], v[e], v[e + 1], a, a, c, c);
+    if constexpr (kMask)
+      m = fmax3(m, e < nvalid ? v[e] : -INFINITY, e + 1 < nvalid ? v[e + 1] : -INFINITY);
+    else
+      m = fmax3(m, v[e], v[e + 1]);
+  }
+#pragma unroll
+  for (int e = 0; e < N; e += 2) {
+    sigma2_fast4(v[e], v[e + 1], v[e], v[e + 1]);
+    // materialise the speculative values here: keeps the compiler from sinking them into the branch
+    // after the vote (which would put the vote back in front of the MUFU work)
+    asm volatile("" : "+f"(v[e]), "+f"(v[e + 1]));
+  }
+  return __all_sync(0xffffffffu, !lane_valid || m <= kFastT4);
+}
+
 // N scores of one row -> N sigma values (in place), choosing the path warp-uniformly.
 // a = alpha log2 e, c = b log2 e (so t = x log2 e = s a + c).  The path vote only looks at valid
 // elements (lane_valid rows, columns < nvalid when kMask): padding can never change which
