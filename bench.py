@@ -45,7 +45,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--workload", default="c3",
-                    help="c3 (BASELINE metric config, default) | c5 (N=16384 B=1 H=16 d=128) | c2:N:d (fwd+bwd, unpadded)")
+                    help="c3 (BASELINE metric config, default) | c4 (one 160M-encoder layer: B=16 H=12 N=8192 d=64) | "
+                         "c5 (N=16384 B=1 H=16 d=128) | c2:N:d (fwd+bwd, unpadded)")
     return ap.parse_args()
 
 
@@ -209,6 +210,8 @@ def main_ours(args):
         cfg = I.C3
     elif args.workload == "c5":
         cfg = I.c5(16, 128)
+    elif args.workload == "c4":
+        cfg = I.c4_layer(0)   # one of the 12 identical-shape attention layers of the 160M encoder
     elif args.workload.startswith("c2:"):
         _, n_, d_ = args.workload.split(":")
         cfg = I.c2(int(n_), int(d_))

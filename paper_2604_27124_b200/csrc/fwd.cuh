@@ -6,12 +6,15 @@
 //   warps 0-15  four sigmoid warpgroups in two pairs that take alternate key tiles (ping-pong: one
 //               pair computes while the other synchronises); within a pair warpgroup g owns key
 //               columns [64g, 64g+64): tcgen05.ld S -> x = alpha s + b -> sigma -> key mask -> bf16
-//               -> tcgen05.st P (aliased onto the first half of its own S columns).  All four
-//               warpgroups then run the epilogue, a quarter of the O columns each (padded query
-//               rows written as exact 0).
+//               -> tcgen05.st P (aliased onto the first half of its own S columns).  The pair
+//               that evaluated an item's last key tile runs its epilogue, half of the O columns
+//               per warpgroup (padded query rows written as exact 0), while the other
+//               pair already evaluates the next item's first tile.
 //   warp 16     TMA producer: Q tile (double-buffered) and a K/V ring of kStages tiles
 //   warp 17     MMA issuer (one elected thread): S = Q K^T (SS, both K-major) -> TMEM S[3] ring
-//                                                O += P V  (TS, P from TMEM, V MN-major) -> TMEM O
+//                                                O += P V  (TS, P from TMEM, V MN-major) -> TMEM O[2]
+//               one stream of key tiles across items: S runs two tiles ahead of PV, also over
+//               item boundaries, and O is double-buffered (D = 64), so nothing drains per q tile
 //   warp 18     TMEM allocator
 // Work items (b, h, q-tile) come from a device work list sorted longest-first (LPT), built
 // by sched.cuh from the device seqlens, so fully padded query tiles are never visited
@@ -59,7 +62,10 @@ struct FwdCfg {
   static constexpr int kKOff = kQOff + 2 * kTileBytes;      // K[kStages]
   static constexpr int kVOff = kKOff + kStages * kTileBytes;
   static constexpr int kBarOff = kVOff + kStages * kTileBytes;
-  static constexpr int kNumBars = 2 + 2 + 4 * kStages + 3 + 3 + 2;
+  // O accumulators: two when TMEM has room (D = 64), so the epilogue of one item overlaps the
+  // first PV of the next
+  static constexpr int kOBufs = (128 * 3 + 2 * D <= 512) ? 2 : 1;
+  static constexpr int kNumBars = 2 + 2 + 4 * kStages + 3 + 3 + 2 * kOBufs;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;  // + alignment slack
   static constexpr int kNumWG = 4;                          // sigmoid warpgroups: warps [0, 4 kNumWG)
   // Single-thread roles sit in the HIGHEST warp ids: the warp scheduler favours high warp ids, so
@@ -72,7 +78,7 @@ struct FwdCfg {
   // S ring of kSBuf 128-column fp32 buffers (P aliased inside each), then O.
   static constexpr uint32_t kSBuf = 3;
   static constexpr uint32_t kColO = 128 * kSBuf;
-  static_assert(kColO + D <= kTmemCols, "TMEM budget");
+  static_assert(kColO + kOBufs * D <= kTmemCols, "TMEM budget");
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -136,8 +142,8 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* v_empty = k_empty + C::kStages;  // V slot free: its PV MMA completed
   uint64_t* s_full = v_empty + C::kStages;   // [kSBuf]
   uint64_t* p_full = s_full + C::kSBuf;      // [kSBuf]
-  uint64_t* o_full = p_full + C::kSBuf;      // [1]
-  uint64_t* o_empty = o_full + 1;            // [1]
+  uint64_t* o_full = p_full + C::kSBuf;      // [kOBufs]
+  uint64_t* o_empty = o_full + C::kOBufs;    // [kOBufs]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -158,8 +164,10 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&k_empty[i], 1);
       sm100::mbar_init(&v_empty[i], 1);
     }
-    sm100::mbar_init(o_full, 1);
-    sm100::mbar_init(o_empty, 4 * C::kNumWG);
+    for (int i = 0; i < C::kOBufs; ++i) {
+      sm100::mbar_init(&o_full[i], 1);
+      sm100::mbar_init(&o_empty[i], 2 * C::kNumWG);   // the 8 warps of the pair that runs the epilogue
+    }
     sm100::fence_barrier_init();
   }
   if (warp == C::kWarpTMA && lane == 0) {
@@ -231,75 +239,90 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
     const uint32_t k_base = sm100::smem_u32(smem + C::kKOff);
     const uint32_t v_base = sm100::smem_u32(smem + C::kVOff);
-    uint32_t kv_it = 0, s_it = 0, c = 0;
-    for (int it = first_item(); it < n_items; it = next_item(it)) {
-      const int nkt = args.items[it].w;
-      if (nkt <= 0) continue;
-      const uint32_t qb = c & 1;
-      sm100::mbar_wait(&q_full[qb], (c >> 1) & 1);
-      const uint32_t qa = q_base + qb * C::kTileBytes;
-      auto issue_s = [&](uint32_t kvi, uint32_t si) {
-        const uint32_t st = kvi % C::kStages;
-        sm100::mbar_wait(&k_full[st], (kvi / C::kStages) & 1);
-        sm100::tc_fence_after();
-        const uint32_t ka = k_base + st * C::kTileBytes;
-        const uint32_t d_s = tmem + (si % C::kSBuf) * 128;
-        if (sm100::elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
-            sm100::mma_ss(d_s, sm100::make_sdesc_sw128(qa + off, 16, 1024),
-                          sm100::make_sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
-          }
-          sm100::mma_commit(&s_full[si % C::kSBuf]);
-          sm100::mma_commit(&k_empty[st]);
-          sm100::trace_event(args.trace, 512 + si, 1024);
-        }
-        __syncwarp();
-      };
-      // S runs two key tiles ahead of PV and is issued BEFORE the PV of the current tile:
-      // S(j+2) reuses the buffer of P(j-1), read by PV(j-1) issued earlier (tcgen05 ops of one
-      // thread execute in order), so it never waits for sigma(j).
-      issue_s(kv_it, s_it);
-      if (nkt > 1) issue_s(kv_it + 1, s_it + 1);
-      for (int j = 0; j < nkt; ++j) {
-        if (j + 2 < nkt) issue_s(kv_it + j + 2, s_it + j + 2);
-        const uint32_t si = s_it + j;
-        sm100::mbar_wait_backoff(&p_full[si % C::kSBuf], (si / C::kSBuf) & 1);
-        if (j == 0) sm100::mbar_wait(o_empty, (c & 1) ^ 1);   // epilogue drained the previous O
-        const uint32_t kvi = kv_it + j;
-        const uint32_t st = kvi % C::kStages;
-        sm100::mbar_wait(&v_full[st], (kvi / C::kStages) & 1);
-        sm100::tc_fence_after();
-        const uint32_t va = v_base + st * C::kTileBytes;
-        const uint32_t p_col = (si % C::kSBuf) * 128;
-        if (sm100::elect_one()) {
-          sm100::trace_event(args.trace, 1024 + si, 1536);
-#pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk) {
-            // P for keys [16kk, 16kk+16): pair warpgroup kk/4 packed its 64 keys at S cols [64 (kk/4), +32)
-            const uint32_t a_col = p_col + (kk >> 2) * 64 + (kk & 3) * 8;
-            sm100::mma_ts(tmem + C::kColO, tmem + a_col,
-                          sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
-                          (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          sm100::mma_commit(&v_empty[st]);
-          sm100::trace_event(args.trace, 1536 + si, 2048);
-        }
-        __syncwarp();
+    // One stream of key tiles over all of this CTA's items: S runs two tiles ahead of PV ACROSS item
+    // boundaries (the next item's Q is double-buffered), so the tensor pipe and the sigmoid warps see
+    // no pipeline drain at the end of a query tile.
+    struct Cur {
+      int it, j, nkt;
+      uint32_t c;   // item ordinal (Q buffer / O buffer parity)
+    };
+    auto skip_empty = [&](Cur& x) {
+      while (x.it < n_items && (x.nkt = args.items[x.it].w) <= 0) x.it = next_item(x.it);
+    };
+    auto advance = [&](Cur& x) {
+      if (++x.j >= x.nkt) {
+        x.j = 0;
+        ++x.c;
+        x.it = next_item(x.it);
+        skip_empty(x);
       }
+    };
+    Cur sc{first_item(), 0, 0, 0};   // next S to issue
+    skip_empty(sc);
+    Cur pc = sc;                     // next PV to issue
+    uint32_t s_it = 0;               // global index of the next S (= K/V ring index, TMEM S buffer)
+    auto issue_s = [&]() {
+      if (sc.it >= n_items) return;
+      const uint32_t qb = sc.c & 1;
+      if (sc.j == 0) sm100::mbar_wait(&q_full[qb], (sc.c >> 1) & 1);
+      const uint32_t qa = q_base + qb * C::kTileBytes;
+      const uint32_t st = s_it % C::kStages;
+      sm100::mbar_wait(&k_full[st], (s_it / C::kStages) & 1);
+      sm100::tc_fence_after();
+      const uint32_t ka = k_base + st * C::kTileBytes;
+      const uint32_t d_s = tmem + (s_it % C::kSBuf) * 128;
       if (sm100::elect_one()) {
-        sm100::mma_commit(&q_empty[qb]);
-        sm100::mma_commit(o_full);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
+          sm100::mma_ss(d_s, sm100::make_sdesc_sw128(qa + off, 16, 1024),
+                        sm100::make_sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
+        }
+        sm100::mma_commit(&s_full[s_it % C::kSBuf]);
+        sm100::mma_commit(&k_empty[st]);
+        sm100::trace_event(args.trace, 512 + s_it, 1024);
       }
       __syncwarp();
-      kv_it += nkt;
-      s_it += nkt;
-      ++c;
+      ++s_it;
+      advance(sc);
+    };
+    // S(g+2) reuses the buffer of P(g-1), read by PV(g-1) issued earlier (tcgen05 ops of one thread
+    // execute in order), so it never waits for sigma(g).
+    issue_s();
+    issue_s();
+    for (uint32_t si = 0; pc.it < n_items; ++si) {
+      issue_s();
+      sm100::mbar_wait_backoff(&p_full[si % C::kSBuf], (si / C::kSBuf) & 1);
+      const uint32_t ob = pc.c % C::kOBufs;
+      if (pc.j == 0) sm100::mbar_wait(&o_empty[ob], ((pc.c / C::kOBufs) & 1) ^ 1);   // epilogue drained this O
+      const uint32_t st = si % C::kStages;
+      sm100::mbar_wait(&v_full[st], (si / C::kStages) & 1);
+      sm100::tc_fence_after();
+      const uint32_t va = v_base + st * C::kTileBytes;
+      const uint32_t p_col = (si % C::kSBuf) * 128;
+      if (sm100::elect_one()) {
+        sm100::trace_event(args.trace, 1024 + si, 1536);
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk) {
+          // P for keys [16kk, 16kk+16): pair warpgroup kk/4 packed its 64 keys at S cols [64 (kk/4), +32)
+          const uint32_t a_col = p_col + (kk >> 2) * 64 + (kk & 3) * 8;
+          sm100::mma_ts(tmem + C::kColO + ob * D, tmem + a_col,
+                        sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
+                        (pc.j > 0 || kk > 0) ? 1u : 0u);
+        }
+        sm100::mma_commit(&v_empty[st]);
+        if (pc.j == pc.nkt - 1) {
+          sm100::mma_commit(&q_empty[pc.c & 1]);
+          sm100::mma_commit(&o_full[ob]);
+        }
+        sm100::trace_event(args.trace, 1536 + si, 2048);
+      }
+      __syncwarp();
+      advance(pc);
     }
   } else if (warp < C::kWarpTMA) {
     // ===================== sigmoid warpgroups + epilogue =====================
-    const uint32_t g = warp >> 2;                // warpgroup (epilogue: O columns [g D/4, (g+1) D/4))
+    const uint32_t g = warp >> 2;                // warpgroup
     const uint32_t pair = warp >> 3;             // warpgroup pair: takes the key tiles with si % 2 == pair
     const uint32_t gp = g & 1;                   // within the pair: key columns [64 gp, 64 gp + 64)
     const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
@@ -319,8 +342,9 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       for (int j = 0; j < nkt; ++j) {
         const uint32_t si = s_it + j;
         if ((si & 1) != pair) continue;          // the other warpgroup pair takes this key tile
+        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 3072 + si, 3584);
         sm100::mbar_wait(&s_full[si % C::kSBuf], (si / C::kSBuf) & 1);
-        if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 2048 + si, 2560);
+        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 2048 + si, 2560);
         sm100::tc_fence_after();
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
@@ -343,49 +367,57 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&p_full[si % C::kSBuf]);
-        if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 2560 + si, 3072);
-        if (lane == 0 && warp == 8) sm100::trace_event(args.trace, 3072 + si, 3584);
+        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 2560 + si, 3072);
       }
+      // ---- epilogue, run by the pair that evaluated the item's last key tile (the other pair goes
+      // straight on to the next item's first tile): O rows of this q tile, columns [gp D/2, +D/2)
+      const uint32_t epi_pair = (s_it + nkt - 1) & 1;
       s_it += nkt;
-      // ---- epilogue: O rows of this q tile, columns [g*D/4, g*D/4 + D/4)
-      sm100::mbar_wait(o_full, c & 1);
-      sm100::tc_fence_after();
-      constexpr int kHalf = D / C::kNumWG;   // columns per warpgroup
-      uint32_t ov[kHalf];
-      if constexpr (kHalf == 32) {
-        sm100::tmem_ld32_sync(tmem + lane_addr + C::kColO + g * kHalf, ov);
-      } else {
-        static_assert(kHalf == 16, "D / kNumWG");
-        sm100::tmem_ld16_sync(tmem + lane_addr + C::kColO + g * kHalf, ov);
-      }
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(o_empty);
-      const int qrow = qt * kTile + (int)row;
-      if (qrow < args.Nq) {
+      if (pair == epi_pair) {
+        const uint32_t ob = c % C::kOBufs;
+        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 3584 + 3 * c, 4094);
+        sm100::mbar_wait(&o_full[ob], (c / C::kOBufs) & 1);
+        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 3584 + 3 * c + 1, 4094);
+        sm100::tc_fence_after();
+        constexpr int kPart = D / 2;   // columns per warpgroup of the pair
+        const uint32_t ocol = C::kColO + ob * D + gp * kPart;
+        const int qrow = qt * kTile + (int)row;
         const bool valid = qrow < nq;
-        const size_t off = ((size_t)(b * args.H + h) * args.Nq + qrow) * D + g * kHalf;
-        if constexpr (kOutF32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + off);
 #pragma unroll
-          for (int e = 0; e < kHalf; e += 4) {
-            float4 w = valid ? make_float4(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1]),
-                                           __uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3]))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-            dst[e >> 2] = w;
+        for (int h0 = 0; h0 < kPart; h0 += 32) {
+          uint32_t ov[32];
+          sm100::tmem_ld32_sync(tmem + lane_addr + ocol + h0, ov);
+          if (h0 + 32 >= kPart) {
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&o_empty[ob]);
           }
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + off);
+          if (qrow < args.Nq) {
+            const size_t off = ((size_t)(b * args.H + h) * args.Nq + qrow) * D + gp * kPart + h0;
+            if constexpr (kOutF32) {
+              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + off);
 #pragma unroll
-          for (int e = 0; e < kHalf; e += 8) {
-            uint4 w;
-            w.x = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 0]), __uint_as_float(ov[e + 1])) : 0u;
-            w.y = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3])) : 0u;
-            w.z = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 4]), __uint_as_float(ov[e + 5])) : 0u;
-            w.w = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 6]), __uint_as_float(ov[e + 7])) : 0u;
-            dst[e >> 3] = w;
+              for (int e = 0; e < 32; e += 4) {
+                float4 w = valid ? make_float4(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1]),
+                                               __uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3]))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+                dst[e >> 2] = w;
+              }
+            } else {
+              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + off);
+#pragma unroll
+              for (int e = 0; e < 32; e += 8) {
+                uint4 w;
+                w.x = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 0]), __uint_as_float(ov[e + 1])) : 0u;
+                w.y = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3])) : 0u;
+                w.z = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 4]), __uint_as_float(ov[e + 5])) : 0u;
+                w.w = valid ? sm100::pack2<kBf16>(__uint_as_float(ov[e + 6]), __uint_as_float(ov[e + 7])) : 0u;
+                dst[e >> 3] = w;
+              }
+            }
           }
         }
+        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 3584 + 3 * c + 2, 4094);
       }
       ++c;
     }

@@ -382,3 +382,77 @@ def test_bias_gradient_autograd():
     o.backward(do)
     ref = oracle.dbias(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, 1 / 8, [-5.0, -4.0, -3.0])
     assert np.abs(bias.grad.double().cpu().numpy() - ref).max() <= 1e-2 * np.abs(ref).max()
+
+
+def _check_sampled(cfg, pairs, q, k, v, do, o, grads, alpha, b, rng, nrand=96):
+    """Sampled rows of the given (b, h) pairs against the row-sampled oracle (exact per row)."""
+    bias = [b]
+    for (bb, hh) in pairs:
+        qs, ks, vs = (f64(t[bb:bb + 1, hh:hh + 1]) for t in (q, k, v))
+        nqb, nkb = [cfg.nq[bb]], [cfg.nk[bb]]
+        rows = _sampled_rows(cfg.nq[bb], cfg.N, rng, k=nrand)
+        checks = [("o", o, oracle.fwd_rows(qs, ks, vs, 0, 0, rows, nqb, nkb, alpha, bias))]
+        if grads is not None:
+            dos = f64(do[bb:bb + 1, hh:hh + 1])
+            dq, dk, dv = grads
+            rdk, rdv = oracle.dkdv_rows(qs, ks, vs, dos, 0, 0, rows, nqb, nkb, alpha, bias)
+            checks += [("dq", dq, oracle.dq_rows(qs, ks, vs, dos, 0, 0, rows, nqb, nkb, alpha, bias)),
+                       ("dk", dk, rdk), ("dv", dv, rdv)]
+        for name, got, ref in checks:
+            err = relerr(f64(got[bb, hh])[rows], ref)
+            assert err <= BF16_TOL, f"{cfg.name} {name} (b={bb}, h={hh}) rel err {err}"
+
+
+@pytest.mark.parametrize("N,d", [(16384, 128), (16384, 64), (1024, 128), (1024, 64)])
+def test_c2_full_size_sampled(N, d):
+    """C2 forward sweep members at full size (B = 16384/N, H = 16, unpadded), in the bench's launch
+    configuration (`bench.py --workload c2:N:d`): sampled rows of two (b, h) pairs."""
+    sa = _sa()
+    cfg = I.c2(N, d)
+    q, k, v, do, nq, nk = I.make_inputs_gpu_fast(cfg, "cuda")
+    alpha, b = 1 / math.sqrt(d), -math.log(N)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(2)
+    _check_sampled(cfg, [(0, 0), (cfg.B - 1, 15)], q, k, v, do, o, None, alpha, b, rng)
+
+
+def test_c4_layer_full_size_sampled():
+    """C4: one 160M-encoder attention layer (B=16, H=12, N=8192, d=64, unpadded) fwd + bwd at full
+    size (`bench.py --workload c4`): sampled rows of three (b, h) pairs."""
+    sa = _sa()
+    cfg = I.c4_layer(0)
+    q, k, v, do, nq, nk = I.make_inputs_gpu_fast(cfg, "cuda")
+    alpha, b = 1 / 8, -math.log(8192)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b)
+    grads = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(3)
+    _check_sampled(cfg, [(0, 0), (7, 5), (15, 11)], q, k, v, do, o, grads, alpha, b, rng, nrand=48)
+
+
+def test_c5_full_size_sampled():
+    """C5: the single 16K sequence (H=16, d=128) fwd + bwd at full size, unsplit (`bench.py --workload
+    c5`), and the same sequence as a G=8 key split (fp32 partials summed), as the CP ranks compute it."""
+    sa = _sa()
+    cfg = I.c5(16, 128)
+    q, k, v, do, nq, nk = I.make_inputs_gpu_fast(cfg, "cuda")
+    alpha, b = 1 / math.sqrt(128), -math.log(16384)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b)
+    grads = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(4)
+    _check_sampled(cfg, [(0, 0), (0, 9)], q, k, v, do, o, grads, alpha, b, rng, nrand=32)
+    # key split over G = 8 shards with the GLOBAL bias: partial fp32 outputs sum to O (P:121)
+    G, blk = 8, 16384 // 8
+    acc = torch.zeros(q.shape, dtype=torch.float32, device="cuda")
+    for r in range(G):
+        ks, vs = k[:, :, r * blk:(r + 1) * blk].contiguous(), v[:, :, r * blk:(r + 1) * blk].contiguous()
+        acc += sa.sigattn_fwd(q, ks, vs, nq, torch.full_like(nk, blk), alpha, b, out_f32=True)
+    torch.cuda.synchronize()
+    rows = _sampled_rows(16384, 16384, rng, k=32)
+    for hh in (0, 9):
+        ref = oracle.fwd_rows(f64(q[:, hh:hh + 1]), f64(k[:, hh:hh + 1]), f64(v[:, hh:hh + 1]), 0, 0, rows,
+                              [16384], [16384], alpha, [b])
+        err = relerr(f64(acc[0, hh])[rows], ref)
+        assert err <= BF16_TOL, f"c5 key-split sum (h={hh}) rel err {err}"
