@@ -64,6 +64,9 @@
 #ifndef SIGATTN_BWD_EMU
 #define SIGATTN_BWD_EMU 0         // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
 #endif
+#ifndef SIGATTN_DBG_NOTMA_QDO
+#define SIGATTN_DBG_NOTMA_QDO 0   // timing experiments only: Q/dO tiles loaded once, then reused (stale)
+#endif
 #ifndef SIGATTN_DBG_MMAONLY
 #define SIGATTN_DBG_MMAONLY 0     // timing experiments only: MMA + TMA pipeline alone (no compute/epilogue waits)
 #endif
@@ -283,9 +286,13 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         const uint32_t st = t % C::kQStages;
         sm100::mbar_wait_backoff(&qdo_empty[st], ((t / C::kQStages) & 1) ^ 1);
         if (sm100::elect_one()) {
-          sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kTileBytes);
-          sm100::tma_load_3d(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q);
-          sm100::tma_load_3d(smem + C::kDOOff + st * C::kTileBytes, &tmDO, &qdo_full[st], 0, i * kTile, zh, pol_q);
+          if (SIGATTN_DBG_NOTMA_QDO && t >= C::kQStages) {   // timing experiments only: stale Q/dO tiles
+            sm100::mbar_arrive(&qdo_full[st]);
+          } else {
+            sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kTileBytes);
+            sm100::tma_load_3d(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q);
+            sm100::tma_load_3d(smem + C::kDOOff + st * C::kTileBytes, &tmDO, &qdo_full[st], 0, i * kTile, zh, pol_q);
+          }
         }
         __syncwarp();
       }
@@ -386,6 +393,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_wait(&dq_empty[qb], ((tq / C::kDQBufs) & 1) ^ 1);   // epilogue drained this accumulator
       sm100::mbar_wait(&ds_full[b2], (tq >> 1) & 1);             // dS(tq) staged in smem, proxy-fenced
 #endif
+      if (lane == 0 && tq >= 40 && tq < 48) sm100::trace_event(args.trace, 3328 + (tq - 40) * 8 + 3, 4094);
       sm100::tc_fence_after();
       if (sm100::elect_one()) {
         const uint32_t ka = k_base + prev_kvb * C::kTileBytes;
@@ -407,6 +415,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       nxt.advance(args.items);
       const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1;
       const uint32_t st1 = (t + 1) % C::kQStages;
+#define MMA_TR(e) if (lane == 0 && t >= 40 && t < 48) sm100::trace_event(args.trace, 3328 + (t - 40) * 8 + (e), 4094)
+      MMA_TR(4);
       // long wait (a compute phase): poll with back-off so the MMA warp does not steal issue slots
 #if !SIGATTN_DBG_MMAONLY
       MMA_WAIT_P(&p_full[0], t & 1);
@@ -418,12 +428,16 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::tc_fence_after();
       if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
       __syncwarp();
+      MMA_TR(0);
       if (nxt.valid) {
         if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
+        MMA_TR(5);
         sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
+        MMA_TR(6);
 #if !SIGATTN_DBG_MMAONLY
         if (kDQ) sm100::mbar_wait(&ds_copied[0], t & 1);   // dS^T(t, q0) left TMEM before S/dP(t+1, q0) land there
 #endif
+        MMA_TR(7);
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
           // the copy executes after every earlier MMA (tcgen05 ops of one thread run in order), so
@@ -448,6 +462,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
       }
       __syncwarp();
+      MMA_TR(1);
       if (nxt.valid) {
 #if !SIGATTN_DBG_MMAONLY
         if (kDQ) sm100::mbar_wait(&ds_copied[1], t & 1);
@@ -456,6 +471,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 1);
         __syncwarp();
       }
+      MMA_TR(2);
       prev_kvb = kvb;
       prev_last = cur.i == cur.nqt - 1;
 #if !SIGATTN_BWD_DQ_LATE
