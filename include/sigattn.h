@@ -56,7 +56,14 @@ enum {
                                           for key-split context parallelism (A4)     */
   SIGATTN_F_DQ_F32_PARTIAL = 1u << 2,  /* bwd: dq is float* fp32 alpha*dS K, not finalised
                                           (for the CP reduce-scatter)                        */
-  SIGATTN_F_NO_ZERO_PAD_OUT = 1u << 3  /* caller does not need padded output rows zeroed     */
+  SIGATTN_F_NO_ZERO_PAD_OUT = 1u << 3, /* caller does not need padded output rows zeroed     */
+  SIGATTN_F_LAYOUT_BSHD = 1u << 4      /* every tensor argument (q, k, v, o, dout, dq, dk, dv)
+                                          is [B, N, H, d] -- the paper's [Z, L, H, D] layout
+                                          (Alg. 1-3 Require lines) --
+                                          instead of [B, H, N, d]; read and written in place
+                                          through strided TMA views, no transposes.  Not
+                                          combinable with SIGATTN_F_DQ_F32_PARTIAL (the CP
+                                          partial dQ is always [B, H, Nq, d]).              */
 };
 
 typedef struct {

@@ -27,20 +27,42 @@ def _dtype_code(t: torch.Tensor) -> int:
     raise TypeError(f"sigattn: dtype {t.dtype} unsupported (bf16 / fp16)")
 
 
-def _check_qkv(q, k, v):
+_LAYOUTS = ("bhsd", "bshd")
+
+
+def _check_qkv(q, k, v, layout: str = "bhsd"):
+    """Returns B, H, Nq, Nk, d.  layout 'bhsd': tensors are [B, H, N, d]; 'bshd': [B, N, H, d], the
+    paper's [Z, L, H, D] -- read in place through strided TMA views."""
+    if layout not in _LAYOUTS:
+        raise ValueError(f"sigattn: layout must be one of {_LAYOUTS}")
     for name, t in (("q", q), ("k", k), ("v", v)):
         if not t.is_cuda:
             raise ValueError(f"sigattn: {name} must be a CUDA tensor (no CPU fallback)")
         if t.dim() != 4:
-            raise ValueError(f"sigattn: {name} must be [B, H, N, d]")
+            raise ValueError(f"sigattn: {name} must be 4-D ({layout})")
         if not t.is_contiguous():
-            raise ValueError(f"sigattn: {name} must be contiguous [B, H, N, d]")
-    B, H, Nq, d = q.shape
-    if k.shape[:2] != (B, H) or k.shape[3] != d or v.shape != k.shape:
-        raise ValueError(f"sigattn: shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+            raise ValueError(f"sigattn: {name} must be contiguous ({layout})")
+    if layout == "bhsd":
+        B, H, Nq, d = q.shape
+        Nk = k.shape[2]
+        ok = k.shape[:2] == (B, H) and k.shape[3] == d
+    else:
+        B, Nq, H, d = q.shape
+        Nk = k.shape[1]
+        ok = k.shape[0] == B and k.shape[2:] == (H, d)
+    if not ok or v.shape != k.shape:
+        raise ValueError(f"sigattn: shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)} ({layout})")
     if k.dtype != q.dtype or v.dtype != q.dtype:
         raise TypeError("sigattn: q, k, v must share a dtype")
-    return B, H, Nq, k.shape[2], d
+    return B, H, Nq, Nk, d
+
+
+def _shape(layout, B, H, N, d):
+    return (B, H, N, d) if layout == "bhsd" else (B, N, H, d)
+
+
+def _layout_flag(layout):
+    return _lib.SIGATTN_F_LAYOUT_BSHD if layout == "bshd" else 0
 
 
 def _lens(t: Optional[torch.Tensor], B: int, device) -> Optional[torch.Tensor]:
@@ -84,20 +106,23 @@ def _stream_handle(device) -> int:
 
 def sigattn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens_q=None, seqlens_k=None,
                 scale: Optional[float] = None, bias: BiasArg = None, out: Optional[torch.Tensor] = None,
-                out_f32: bool = False, zero_pad_out: bool = True) -> torch.Tensor:
-    """Forward (Alg. 1).  Returns O [B, H, Nq, d] in q.dtype (fp32 if out_f32: a CP partial)."""
+                out_f32: bool = False, zero_pad_out: bool = True, layout: str = "bhsd") -> torch.Tensor:
+    """Forward (Alg. 1).  Returns O [B, H, Nq, d] ([B, Nq, H, d] for layout='bshd') in q.dtype
+    (fp32 if out_f32: a CP partial)."""
     lib = _lib.load()
-    B, H, Nq, Nk, d = _check_qkv(q, k, v)
+    B, H, Nq, Nk, d = _check_qkv(q, k, v, layout)
     sq = _lens(seqlens_q, B, q.device)
     sk = _lens(seqlens_k, B, q.device) if seqlens_k is not None else sq if Nk == Nq else None
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     b_scalar, b_tensor = resolve_bias(bias, Nk, sk, B, q.device)
     odt = torch.float32 if out_f32 else q.dtype
+    oshape = _shape(layout, B, H, Nq, d)
     if out is None:
-        out = torch.empty((B, H, Nq, d), dtype=odt, device=q.device)
-    elif out.shape != (B, H, Nq, d) or out.dtype != odt or not out.is_contiguous():
+        out = torch.empty(oshape, dtype=odt, device=q.device)
+    elif out.shape != oshape or out.dtype != odt or not out.is_contiguous():
         raise ValueError("sigattn: bad out tensor")
-    flags = (_lib.SIGATTN_F_OUT_F32_PARTIAL if out_f32 else 0) | (0 if zero_pad_out else _lib.SIGATTN_F_NO_ZERO_PAD_OUT)
+    flags = ((_lib.SIGATTN_F_OUT_F32_PARTIAL if out_f32 else 0) | (0 if zero_pad_out else _lib.SIGATTN_F_NO_ZERO_PAD_OUT)
+             | _layout_flag(layout))
     p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags)
     _lib.check(lib.sigattn_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                _stream_handle(q.device)))
@@ -112,7 +137,7 @@ def bwd_workspace_bytes(B, H, Nq, Nk, d, dtype=torch.bfloat16) -> int:
 
 def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias: BiasArg = None,
                 dq=None, dk=None, dv=None, workspace: Optional[torch.Tensor] = None, dq_f32: bool = False,
-                deterministic: bool = False, dbias: Optional[torch.Tensor] = None):
+                deterministic: bool = False, dbias: Optional[torch.Tensor] = None, layout: str = "bhsd"):
     """Backward (Alg. 2 + Alg. 3, fused).  Returns (dQ, dK, dV); dQ is fp32 if dq_f32 (CP partial).
 
     deterministic=True runs the paper's two passes instead (dK/dV key-tile-owned, dQ
@@ -121,17 +146,21 @@ def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias:
     dS_ij -- the gradient of a learnable per-sequence bias.
     """
     lib = _lib.load()
-    B, H, Nq, Nk, d = _check_qkv(q, k, v)
+    B, H, Nq, Nk, d = _check_qkv(q, k, v, layout)
+    if dq_f32 and layout != "bhsd":
+        raise ValueError("sigattn: dq_f32 (CP partial) needs layout='bhsd'")
     if dout.shape != q.shape or dout.dtype != q.dtype or not dout.is_contiguous():
         raise ValueError("sigattn: dout must match q")
     sq = _lens(seqlens_q, B, q.device)
     sk = _lens(seqlens_k, B, q.device) if seqlens_k is not None else sq if Nk == Nq else None
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     b_scalar, b_tensor = resolve_bias(bias, Nk, sk, B, q.device)
-    dq = torch.empty((B, H, Nq, d), dtype=torch.float32 if dq_f32 else q.dtype, device=q.device) if dq is None else dq
+    dq = torch.empty(_shape(layout, B, H, Nq, d), dtype=torch.float32 if dq_f32 else q.dtype,
+                     device=q.device) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
-    flags = (_lib.SIGATTN_F_DQ_F32_PARTIAL if dq_f32 else 0) | (_lib.SIGATTN_F_BWD_DETERMINISTIC if deterministic else 0)
+    flags = ((_lib.SIGATTN_F_DQ_F32_PARTIAL if dq_f32 else 0) | (_lib.SIGATTN_F_BWD_DETERMINISTIC if deterministic else 0)
+             | _layout_flag(layout))
     if dbias is not None and (dbias.dtype != torch.float32 or dbias.numel() != B or not dbias.is_contiguous()
                               or not dbias.is_cuda):
         raise ValueError("sigattn: dbias must be a contiguous fp32 CUDA tensor with B entries")
@@ -189,8 +218,9 @@ class SigmoidAttentionFn(torch.autograd.Function):
     """Autograd op: saves q, k, v and the lengths -- never O or P (P is recomputed)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, seqlens_q, seqlens_k, scale, bias, deterministic=False):
-        o = sigattn_fwd(q, k, v, seqlens_q, seqlens_k, scale, bias)
+    def forward(ctx, q, k, v, seqlens_q, seqlens_k, scale, bias, deterministic=False, layout="bhsd"):
+        o = sigattn_fwd(q, k, v, seqlens_q, seqlens_k, scale, bias, layout=layout)
+        ctx.layout = layout
         ctx.save_for_backward(q, k, v, seqlens_q, seqlens_k, bias if isinstance(bias, torch.Tensor) else None)
         ctx.scale = scale
         ctx.bias = None if isinstance(bias, torch.Tensor) else bias
@@ -205,29 +235,32 @@ class SigmoidAttentionFn(torch.autograd.Function):
         bias = bt if bt is not None else ctx.bias
         db = torch.empty(q.shape[0], dtype=torch.float32, device=q.device) if ctx.bias_grad else None
         dq, dk, dv = sigattn_bwd(q, k, v, do.contiguous(), sq, sk, ctx.scale, bias,
-                                 deterministic=ctx.deterministic, dbias=db)
+                                 deterministic=ctx.deterministic, dbias=db, layout=ctx.layout)
         dbias = db.to(bt.dtype).reshape(bt.shape) if db is not None else None
-        return dq, dk, dv, None, None, None, dbias, None
+        return dq, dk, dv, None, None, None, dbias, None, None
 
 
 def sigmoid_attention(q, k, v, seqlens_q=None, seqlens_k=None, key_padding_mask=None,
-                      scale: Optional[float] = None, bias: BiasArg = None, deterministic: bool = False):
+                      scale: Optional[float] = None, bias: BiasArg = None, deterministic: bool = False,
+                      layout: str = "bhsd"):
     """O = sigma(scale * Q K^T + bias) V with padded keys at zero weight; differentiable.
 
     deterministic=True selects the paper's two-pass backward (bitwise reproducible dQ).
 
-    q [B,H,Nq,d], k/v [B,H,Nk,d] (bf16/fp16, CUDA, contiguous).  Lengths as int32 [B] tensors,
-    or a PyTorch key_padding_mask [B, Nk] (True = pad; prefix masks only).
+    q [B,H,Nq,d], k/v [B,H,Nk,d] (bf16/fp16, CUDA, contiguous) -- or, with layout='bshd', the
+    paper's [B,N,H,d].  Lengths as int32 [B] tensors, or a PyTorch key_padding_mask [B, Nk]
+    (True = pad; prefix masks only).
     """
+    ndim = 2 if layout == "bhsd" else 1
     if key_padding_mask is not None:
         if seqlens_k is not None:
             raise ValueError("give seqlens or key_padding_mask, not both")
         seqlens_k = sigattn_mask_to_seqlens(key_padding_mask)
-        if seqlens_q is None and q.shape[2] == k.shape[2]:
+        if seqlens_q is None and q.shape[ndim] == k.shape[ndim]:
             seqlens_q = seqlens_k
     B = q.shape[0]
     sq = _lens(seqlens_q, B, q.device)
     sk = _lens(seqlens_k, B, q.device)
-    if sk is None and sq is not None and q.shape[2] == k.shape[2]:
+    if sk is None and sq is not None and q.shape[ndim] == k.shape[ndim]:
         sk = sq
-    return SigmoidAttentionFn.apply(q, k, v, sq, sk, scale, bias, deterministic)
+    return SigmoidAttentionFn.apply(q, k, v, sq, sk, scale, bias, deterministic, layout)

@@ -97,6 +97,7 @@ struct BwdArgs {
   void* dq_pad;           // 16-bit dQ output whose rows >= ceil128(n_q) the fill warp zeroes, or nullptr
   float* dbias;           // [B] fp32, zeroed at entry, += sum of dS (learnable bias gradient); or nullptr
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots (8 events x 512 tiles)
+  int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
 };
 
 template <int D>
@@ -200,7 +201,9 @@ __device__ __forceinline__ void dbias_flush(float* dbias, int b, float acc, uint
 
 // kDQ = false: dK, dV only (the key-tile-owned pass of the deterministic backward, Alg. 3;
 // dQ then comes from sigattn_dq_kernel, Alg. 2): no dQ MMA, no dS staging, no dQ reduction.
-template <int D, bool kBf16, bool kDQ = true, bool kDB = false>
+// kBSHD: tensors are [B, N, H, d] -- a template flag here (the d = 64 backward runs at the
+// register limit; a runtime layout test cost 2% through extra spills)
+template <int D, bool kBf16, bool kDQ = true, bool kDB = false, bool kBSHD = false>
 __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
 sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -278,8 +281,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_wait_backoff(&kv_empty[kvb], ((kv_c >> 1) & 1) ^ 1);
       if (sm100::elect_one()) {
         sm100::mbar_arrive_expect_tx(&kv_full[kvb], 2 * C::kTileBytes);
-        sm100::tma_load_3d(smem + C::kKOff + kvb * C::kTileBytes, &tmK, &kv_full[kvb], 0, kt * kTile, zh, pol_kv);
-        sm100::tma_load_3d(smem + C::kVOff + kvb * C::kTileBytes, &tmV, &kv_full[kvb], 0, kt * kTile, zh, pol_kv);
+        sm100::tma_load_bh(smem + C::kKOff + kvb * C::kTileBytes, &tmK, &kv_full[kvb], 0, kt * kTile, zh, pol_kv, kBSHD ? args.H : 0);
+        sm100::tma_load_bh(smem + C::kVOff + kvb * C::kTileBytes, &tmV, &kv_full[kvb], 0, kt * kTile, zh, pol_kv, kBSHD ? args.H : 0);
       }
       __syncwarp();
       for (int i = 0; i < nqt; ++i, ++t) {
@@ -290,8 +293,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             sm100::mbar_arrive(&qdo_full[st]);
           } else {
             sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kTileBytes);
-            sm100::tma_load_3d(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q);
-            sm100::tma_load_3d(smem + C::kDOOff + st * C::kTileBytes, &tmDO, &qdo_full[st], 0, i * kTile, zh, pol_q);
+            sm100::tma_load_bh(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q, kBSHD ? args.H : 0);
+            sm100::tma_load_bh(smem + C::kDOOff + st * C::kTileBytes, &tmDO, &qdo_full[st], 0, i * kTile, zh, pol_q, kBSHD ? args.H : 0);
           }
         }
         __syncwarp();
@@ -659,7 +662,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::tc_fence_after();
       const int key = kt * kTile + (int)row;
       const bool key_valid = key < nk;
-      const size_t off = (zh * args.Nk + key) * D;
+      const size_t off = kBSHD ? row_off(1, args.H, args.Nk, D, b, h, key) : (zh * args.Nk + key) * D;
 #pragma unroll
       for (int which = 0; which < 2; ++which) {
         const uint32_t col = which == 0 ? C::kColDV : C::kColDK;
@@ -703,10 +706,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   }
 
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
-    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
-    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
+    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0);
+    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0);
     if (args.dq_pad)   // dq_finalize_kernel covers the rows below
-      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane);
+      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, kBSHD ? 1 : 0);
   }
 
   sm100::tc_fence_before();

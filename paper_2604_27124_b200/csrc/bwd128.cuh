@@ -118,8 +118,8 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sm100::mbar_arrive_expect_tx(kv_full, 2 * C::kKVBytes);
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-          sm100::tma_load_3d(smem + C::kKOff + s * (kTile * 128), &tmK, kv_full, s * 64, kt * kTile, zh, pol_kv);
-          sm100::tma_load_3d(smem + C::kVOff + s * (kTile * 128), &tmV, kv_full, s * 64, kt * kTile, zh, pol_kv);
+          sm100::tma_load_bh(smem + C::kKOff + s * (kTile * 128), &tmK, kv_full, s * 64, kt * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+          sm100::tma_load_bh(smem + C::kVOff + s * (kTile * 128), &tmV, kv_full, s * 64, kt * kTile, zh, pol_kv, args.bshd ? args.H : 0);
         }
       }
       __syncwarp();
@@ -130,10 +130,10 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
           sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kQBytes);
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
-            sm100::tma_load_3d(smem + C::kQOff + st * C::kQBytes + s * (C::kQT * 128), &tmQ, &qdo_full[st], s * 64,
-                               i * C::kQT, zh, pol_q);
-            sm100::tma_load_3d(smem + C::kDOOff + st * C::kQBytes + s * (C::kQT * 128), &tmDO, &qdo_full[st],
-                               s * 64, i * C::kQT, zh, pol_q);
+            sm100::tma_load_bh(smem + C::kQOff + st * C::kQBytes + s * (C::kQT * 128), &tmQ, &qdo_full[st], s * 64,
+                               i * C::kQT, zh, pol_q, args.bshd ? args.H : 0);
+            sm100::tma_load_bh(smem + C::kDOOff + st * C::kQBytes + s * (C::kQT * 128), &tmDO, &qdo_full[st],
+                               s * 64, i * C::kQT, zh, pol_q, args.bshd ? args.H : 0);
           }
         }
         __syncwarp();
@@ -325,7 +325,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       sm100::tc_fence_after();
       const int key = kt * kTile + (int)row;
       const bool key_valid = key < nk;
-      const size_t off = (zh * args.Nk + key) * D;
+      const size_t off = args.bshd ? row_off(1, args.H, args.Nk, D, b, h, key) : (zh * args.Nk + key) * D;
 #pragma unroll 1
       for (int which = 0; which < 2; ++which) {
         const uint32_t col0 = which == 0 ? C::kColDV : C::kColDK;
@@ -363,10 +363,10 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
   }
 
   if (warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
-    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
-    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane);
+    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, args.bshd);
+    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, args.bshd);
     if (args.dq_pad)   // dq_finalize_kernel covers the rows below
-      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane);
+      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, args.bshd);
   }
 
   sm100::tc_fence_before();

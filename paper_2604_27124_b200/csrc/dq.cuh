@@ -33,6 +33,7 @@ struct DqArgs {
   float scale;
   int B, H, Nq, Nk;
   void* dq;               // bf16/fp16 [B,H,Nq,D], or fp32 when kOutF32 (context-parallel partial)
+  int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
 };
 
 template <int D>
@@ -131,10 +132,10 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         sm100::mbar_arrive_expect_tx(&q_full[qb], 2 * C::kTileBytes);
 #pragma unroll
         for (int s = 0; s < C::kSub; ++s) {
-          sm100::tma_load_3d(smem + C::kQOff + qb * C::kTileBytes + s * (kTile * 128), &tmQ, &q_full[qb], s * 64,
-                             qt * kTile, zh, pol_q);
-          sm100::tma_load_3d(smem + C::kDOOff + qb * C::kTileBytes + s * (kTile * 128), &tmDO, &q_full[qb],
-                             s * 64, qt * kTile, zh, pol_q);
+          sm100::tma_load_bh(smem + C::kQOff + qb * C::kTileBytes + s * (kTile * 128), &tmQ, &q_full[qb], s * 64,
+                             qt * kTile, zh, pol_q, args.bshd ? args.H : 0);
+          sm100::tma_load_bh(smem + C::kDOOff + qb * C::kTileBytes + s * (kTile * 128), &tmDO, &q_full[qb],
+                             s * 64, qt * kTile, zh, pol_q, args.bshd ? args.H : 0);
         }
       }
       __syncwarp();
@@ -145,8 +146,8 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
           sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_3d(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
-                               j * kTile, zh, pol_kv);
+            sm100::tma_load_bh(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
+                               j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
         }
         __syncwarp();
         sm100::mbar_wait_backoff(&v_empty[st], ph ^ 1);
@@ -154,8 +155,8 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
           sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_3d(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
-                               j * kTile, zh, pol_kv);
+            sm100::tma_load_bh(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
+                               j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
         }
         __syncwarp();
       }
@@ -300,7 +301,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
       if (qrow < args.Nq) {
         const bool valid = qrow < nq;
         const float alpha = args.scale;
-        const size_t off = ((size_t)(b * args.H + h) * args.Nq + qrow) * D + g * kPart;
+        const size_t off = row_off(args.bshd, args.H, args.Nq, D, b, h, qrow) + g * kPart;
         if constexpr (kOutF32) {
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.dq) + off);
 #pragma unroll
@@ -327,7 +328,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill)   // padded dQ rows beyond the last valid tile
     pad_fill_warp(args.dq, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
-                  kTile, lane);
+                  kTile, lane, args.bshd);
 
   sm100::tc_fence_before();
   __syncthreads();

@@ -51,6 +51,7 @@ struct FwdArgs {
   void* o;                // bf16/fp16 [B,H,Nq,D] or fp32 partial
   int fill_pad;           // zero the O rows no tile epilogue writes (pad_fill_warp)
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots
+  int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
 };
 
 template <int D>
@@ -203,7 +204,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         uint8_t* qs = smem + C::kQOff + qb * C::kTileBytes;
 #pragma unroll
         for (int s = 0; s < C::kSub; ++s)
-          sm100::tma_load_3d(qs + s * (kTile * 128), &tmQ, &q_full[qb], s * 64, qt * kTile, zh, pol_q);
+          sm100::tma_load_bh(qs + s * (kTile * 128), &tmQ, &q_full[qb], s * 64, qt * kTile, zh, pol_q, args.bshd ? args.H : 0);
       }
       __syncwarp();
       for (int j = 0; j < nkt; ++j, ++kv_it) {
@@ -217,7 +218,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_3d(ks + s * (kTile * 128), &tmK, &k_full[st], s * 64, j * kTile, zh, pol_kv);
+            sm100::tma_load_bh(ks + s * (kTile * 128), &tmK, &k_full[st], s * 64, j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
         }
         __syncwarp();
         sm100::mbar_wait_backoff(&v_empty[st], ph ^ 1);
@@ -226,7 +227,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_3d(vs + s * (kTile * 128), &tmV, &v_full[st], s * 64, j * kTile, zh, pol_kv);
+            sm100::tma_load_bh(vs + s * (kTile * 128), &tmV, &v_full[st], s * 64, j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
         }
         __syncwarp();
       }
@@ -393,7 +394,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             if (lane == 0) sm100::mbar_arrive(&o_empty[ob]);
           }
           if (qrow < args.Nq) {
-            const size_t off = ((size_t)(b * args.H + h) * args.Nq + qrow) * D + gp * kPart + h0;
+            const size_t off = row_off(args.bshd, args.H, args.Nq, D, b, h, qrow) + gp * kPart + h0;
             if constexpr (kOutF32) {
               float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + off);
 #pragma unroll
@@ -425,7 +426,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill && args.fill_pad)   // padded O rows beyond the last valid tile
     pad_fill_warp(args.o, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
-                  128, lane);
+                  128, lane, args.bshd);
 
   sm100::tc_fence_before();
   __syncthreads();

@@ -126,8 +126,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         for (int x = 0; x < ntq; ++x)
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_3d(smem + C::kQOff + (qb * 2 + x) * C::kTileBytes + s * (kTile * 128), &tmQ, &q_full[qb],
-                               s * 64, (2 * pi + x) * kTile, zh, pol_q);
+            sm100::tma_load_bh(smem + C::kQOff + (qb * 2 + x) * C::kTileBytes + s * (kTile * 128), &tmQ, &q_full[qb],
+                               s * 64, (2 * pi + x) * kTile, zh, pol_q, args.bshd ? args.H : 0);
       }
       __syncwarp();
       for (int j = 0; j < nkt; ++j, ++kv_it) {
@@ -137,8 +137,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
           sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_3d(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
-                               j * kTile, zh, pol_kv);
+            sm100::tma_load_bh(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
+                               j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
         }
         __syncwarp();
         sm100::mbar_wait_backoff(&v_empty[st], ph ^ 1);
@@ -146,8 +146,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
           sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_3d(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
-                               j * kTile, zh, pol_kv);
+            sm100::tma_load_bh(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
+                               j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
         }
         __syncwarp();
       }
@@ -301,7 +301,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
       sm100::tc_fence_after();
       const int qrow = qt * kTile + (int)row;
       const bool valid = qrow < nq;
-      const size_t rowoff = ((size_t)(b * args.H + h) * args.Nq + qrow) * D;
+      const size_t rowoff = row_off(args.bshd, args.H, args.Nq, D, b, h, qrow);
 #pragma unroll
       for (int pc = 0; pc < D / 64; ++pc) {
         const int c0 = (int)gp * (D / 2) + pc * 32;
@@ -340,7 +340,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill && args.fill_pad)   // padded O rows beyond the last valid tile
     pad_fill_warp(args.o, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
-                  kTile, lane);
+                  kTile, lane, args.bshd);
 
   sm100::tc_fence_before();
   __syncthreads();

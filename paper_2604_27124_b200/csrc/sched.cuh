@@ -127,23 +127,40 @@ bwd_prep_kernel(int B, int H, int Nq, int Nk, int D, const int32_t* __restrict__
   }
 }
 
-// One warp zeroes, for every (b, h) slab it is given, rows [r0, N) of a [B*H, N, row_bytes] tensor:
+// Element offset of row `row` of the (b, h) slab of a [B, H, N, D] (bshd = 0) or [B, N, H, D]
+// (bshd = 1, the paper's [Z, L, H, D] layout) tensor.
+__device__ __forceinline__ size_t row_off(int bshd, int H, int N, int D, int b, int h, int row) {
+  return bshd ? ((size_t)((size_t)b * N + row) * H + h) * D : ((size_t)((size_t)b * H + h) * N + row) * D;
+}
+
+// One warp zeroes, for every (b, h) slab it is given, rows [r0, N) of a [B, H, N, row] (or, with
+// bshd, [B, N, H, row]) tensor of row_bytes-long rows:
 // r0 = 0 when the sequence has no work item (n_own == 0 or n_other == 0), else min(ceil_gran(n_own), N)
 // -- the rows below r0 are written (padded rows as zeros) by the tile epilogues.  Slabs are strided
 // over the grid; the idle warp of each persistent attention CTA runs this alongside the main work.
 __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, int H, int N,
                                               const int32_t* __restrict__ lens_own,
                                               const int32_t* __restrict__ lens_other, int N_other, int gran,
-                                              uint32_t lane) {
+                                              uint32_t lane, int bshd = 0) {
   const uint4 z = make_uint4(0, 0, 0, 0);
+  const int cpr = row_bytes / 16;   // 16-byte chunks per row
   for (int zh = blockIdx.x; zh < B * H; zh += gridDim.x) {
-    const int b = zh / H;
+    const int b = zh / H, h = zh - b * H;
     const int n = clamp_len(lens_own, b, N), m = clamp_len(lens_other, b, N_other);
     const int r0 = (n == 0 || m == 0) ? 0 : min((n + gran - 1) / gran * gran, N);
     if (r0 >= N) continue;
-    uint4* base = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out) + ((size_t)zh * N + r0) * row_bytes);
-    const long long total = (long long)(N - r0) * (row_bytes / 16);
-    for (long long i = lane; i < total; i += 32) base[i] = z;
+    if (!bshd) {
+      const long long total = (long long)(N - r0) * cpr;
+      uint4* base = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out) + ((size_t)zh * N + r0) * row_bytes);
+      for (long long i = lane; i < total; i += 32) base[i] = z;
+    } else {
+      // row r of slab (b, h) starts at ((b N + r) H + h) row_bytes; cpr divides 32 (row_bytes is
+      // 128, 256 or 512): each lane owns one 16-byte chunk of every (32 / cpr)-th row
+      uint8_t* base = reinterpret_cast<uint8_t*>(out) + ((size_t)b * N * H + h) * row_bytes;
+      const size_t rs = (size_t)H * row_bytes;
+      const int step = 32 / cpr, lr = (int)lane / cpr, c = (int)lane % cpr;
+      for (int r = r0 + lr; r < N; r += step) reinterpret_cast<uint4*>(base + (size_t)r * rs)[c] = z;
+    }
   }
 }
 
@@ -151,7 +168,7 @@ __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, i
 // dq[r] = r < n_q ? round(acc[r]) : 0.  (acc rows are read through L2, ld.global.cg.)
 template <bool kBf16>
 __device__ __forceinline__ void dq_finalize_rows(const float* __restrict__ acc, uint16_t* __restrict__ dq, int D,
-                                                 int r0, int r1, int nq, uint32_t lane) {
+                                                 int r0, int r1, int nq, uint32_t lane, size_t dq_rs) {
   const int v8 = D / 8;
   const long long total = (long long)(r1 - r0) * v8;
   for (long long i = lane; i < total; i += 32) {
@@ -173,7 +190,7 @@ __device__ __forceinline__ void dq_finalize_rows(const float* __restrict__ acc, 
         asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(w.w) : "f"(c.w), "f"(c.z));
       }
     }
-    *reinterpret_cast<uint4*>(dq + e) = w;
+    *reinterpret_cast<uint4*>(dq + (size_t)r * dq_rs + (i % v8) * 8) = w;
   }
 }
 
@@ -182,7 +199,8 @@ __device__ __forceinline__ void dq_finalize_rows(const float* __restrict__ acc, 
 // dq[b,h,i,:] = i < n_q[b] ? round(acc[b,h,i,:]) : 0    (acc already holds alpha * dS K)
 template <bool kBf16>
 __global__ void dq_finalize_kernel(const float* __restrict__ acc, uint16_t* __restrict__ dq, int H, int N, int D,
-                                   const int32_t* __restrict__ lens, const int32_t* __restrict__ lens_k, int Nk) {
+                                   const int32_t* __restrict__ lens, const int32_t* __restrict__ lens_k, int Nk,
+                                   int bshd) {
   const int zh = blockIdx.y;
   const int nq = clamp_len(lens, zh / H, N), nk = clamp_len(lens_k, zh / H, Nk);
   // rows from ceil128(n_q) on (all rows if the sequence has no work) are zeroed by the backward
@@ -194,7 +212,8 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, uint16_t* __re
   const int per = (r1 - r0 + nwarps - 1) / nwarps;
   const int w0 = r0 + warp * per, w1 = min(r1, w0 + per);
   if (w0 < w1)
-    dq_finalize_rows<kBf16>(acc + (size_t)zh * N * D, dq + (size_t)zh * N * D, D, w0, w1, nq, threadIdx.x & 31);
+    dq_finalize_rows<kBf16>(acc + (size_t)zh * N * D, dq + row_off(bshd, H, N, D, zh / H, zh % H, 0), D, w0, w1, nq,
+                            threadIdx.x & 31, bshd ? (size_t)H * D : (size_t)D);
 }
 
 // key_padding_mask [B, N] (1 = pad) -> seqlens[b] = number of valid tokens; flags non-prefix masks.

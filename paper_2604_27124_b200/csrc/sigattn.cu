@@ -74,22 +74,29 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-// 3-D view {d (inner), rows, B*H} of a [B, H, rows, d] tensor; box {64 elements = 128 B, 128, 1},
-// 128-byte swizzle: exactly the UMMA K-major / MN-major SWIZZLE_128B atom.  Rows past `rows`
-// read as zero (OOB fill), so a ragged last tile never touches another head's data.
+// [B, H, rows, d] tensor: 3-D view {d (inner), rows, B H}.  With bshd, the paper's [B, rows, H, d]
+// layout: 4-D view {d, rows, H, B}.  Box {64 elements = 128 B, box_rows, 1(, 1)}, 128-byte
+// swizzle: exactly the UMMA K-major / MN-major SWIZZLE_128B atom whichever the layout.  Rows past
+// `rows` read as zero (OOB fill), so a ragged last tile never touches another head's or sequence's data.
 sigattn_status make_tmap(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int elem_bytes, int d, int rows,
-                         int bh, int box_rows = 128) {
+                         int B, int H, bool bshd, int box_rows = 128) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(SIGATTN_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
-  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)bh};
-  cuuint64_t strides[2] = {(cuuint64_t)d * elem_bytes, (cuuint64_t)d * elem_bytes * rows};
-  cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const cuuint64_t e = (cuuint64_t)elem_bytes, dd = (cuuint64_t)d, n = (cuuint64_t)rows, hh = (cuuint64_t)H;
+  cuuint64_t dims[4] = {dd, n, bshd ? hh : hh * (cuuint64_t)B, (cuuint64_t)B};
+  cuuint64_t strides[3] = {bshd ? hh * dd * e : dd * e,    // next row
+                           bshd ? dd * e : n * dd * e,     // next head ((b, h) slab without bshd)
+                           n * hh * dd * e};               // next sequence (bshd only)
+  cuuint32_t box[4] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, dt, bshd ? 4 : 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SIGATTN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return SIGATTN_OK;
 }
+
+bool layout_bshd(const sigattn_params* p) { return (p->flags & SIGATTN_F_LAYOUT_BSHD) != 0; }
 
 int num_sms() {
   int dev = 0, n = 148;
@@ -156,11 +163,10 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
                           const int4* items, const int* n_items, int max_items, cudaStream_t s) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv;
-  const int bh = p->B * p->H;
   sigattn_status st;
-  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
   FwdArgs a;
   a.items = items;
   a.n_items = n_items;
@@ -176,6 +182,7 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   a.o = o;
   a.fill_pad = (p->flags & SIGATTN_F_NO_ZERO_PAD_OUT) ? 0 : 1;
   a.trace = g_trace;
+  a.bshd = layout_bshd(p) ? 1 : 0;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   if constexpr (use_fwd2(D)) {
     using C = Fwd2Cfg<D>;
@@ -203,15 +210,14 @@ sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* 
                           void* dq_pad = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
-  const int bh = p->B * p->H;
   sigattn_status st;
-  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
   CUtensorMap tdq;   // fp32 dQ accumulator, 32-column boxes for the TMA reduce-add
   std::memset(&tdq, 0, sizeof(tdq));
-  if (kDQ && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, bh)) != SIGATTN_OK)
+  if (kDQ && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, p->B, p->H, false)) != SIGATTN_OK)
     return st;
   BwdArgs a;
   a.items = items;
@@ -231,8 +237,9 @@ sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* 
   a.dq_pad = dq_pad;
   a.dbias = p->dbias;
   a.trace = g_trace;
+  a.bshd = layout_bshd(p) ? 1 : 0;
   using C = BwdCfg<D>;
-  auto kern = sigattn_bwd_kernel<D, kBf16, kDQ, kDB>;
+  auto kern = layout_bshd(p) ? sigattn_bwd_kernel<D, kBf16, kDQ, kDB, true> : sigattn_bwd_kernel<D, kBf16, kDQ, kDB, false>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);
@@ -250,12 +257,11 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
                              void* dq_pad = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
-  const int bh = p->B * p->H;
   sigattn_status st;
-  if ((st = make_tmap(&tq, q, dt, 2, 128, p->Nq, bh, Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tk, k, dt, 2, 128, p->Nk, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tv, v, dt, 2, 128, p->Nk, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tdo, dout, dt, 2, 128, p->Nq, bh, Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tq, q, dt, 2, 128, p->Nq, p->B, p->H, layout_bshd(p), Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tk, k, dt, 2, 128, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tv, v, dt, 2, 128, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tdo, dout, dt, 2, 128, p->Nq, p->B, p->H, layout_bshd(p), Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
   BwdArgs a;
   a.items = items;
   a.n_items = n_items;
@@ -274,6 +280,7 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   a.dq_pad = dq_pad;
   a.dbias = p->dbias;
   a.trace = g_trace;
+  a.bshd = layout_bshd(p) ? 1 : 0;
   auto kern = sigattn_bwd128_kernel<kBf16, kDQ, kDB>;
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
@@ -306,12 +313,11 @@ sigattn_status launch_dq(const sigattn_params* p, const void* q, const void* k, 
                          void* dq, const int4* items, const int* n_items, int max_items, cudaStream_t s) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
-  const int bh = p->B * p->H;
   sigattn_status st;
-  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, bh)) != SIGATTN_OK) return st;
-  if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, bh)) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tq, q, dt, 2, D, p->Nq, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tk, k, dt, 2, D, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tv, v, dt, 2, D, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
+  if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
   DqArgs a;
   a.items = items;
   a.n_items = n_items;
@@ -325,6 +331,7 @@ sigattn_status launch_dq(const sigattn_params* p, const void* q, const void* k, 
   a.Nq = p->Nq;
   a.Nk = p->Nk;
   a.dq = dq;
+  a.bshd = layout_bshd(p) ? 1 : 0;
   using C = DqCfg<D>;
   auto kern = sigattn_dq_kernel<D, kBf16, kF32>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
@@ -481,6 +488,8 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
     return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool dq_f32 = (p->flags & SIGATTN_F_DQ_F32_PARTIAL) != 0;
+  if (dq_f32 && layout_bshd(p))
+    return fail(SIGATTN_EUNSUPPORTED, "SIGATTN_F_DQ_F32_PARTIAL needs the [B, H, N, d] layout");
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   const bool bf = p->dtype == SIGATTN_BF16;
   if (p->flags & SIGATTN_F_BWD_DETERMINISTIC) {
@@ -533,10 +542,10 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   const dim3 grid(std::max(1, std::min(32, cdiv(p->Nq, 512))), p->B * p->H);
   if (bf)
     dq_finalize_kernel<true><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
-                                                  p->seqlens_q, p->seqlens_k, p->Nk);
+                                                  p->seqlens_q, p->seqlens_k, p->Nk, layout_bshd(p) ? 1 : 0);
   else
     dq_finalize_kernel<false><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
-                                                   p->seqlens_q, p->seqlens_k, p->Nk);
+                                                   p->seqlens_q, p->seqlens_k, p->Nk, layout_bshd(p) ? 1 : 0);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;

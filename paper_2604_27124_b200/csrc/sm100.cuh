@@ -153,6 +153,22 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(cache_hint)
       : "memory");
 }
+// Tiled load of the (b, h) slab zh = b H + h at coordinates (c0, c1): bshd_h == 0 -> the 3-D
+// {d, rows, B H} view of a [B, H, N, d] tensor; bshd_h == H -> the 4-D {d, rows, H, B} view of the
+// paper's [B, N, H, d] layout.
+__device__ __forceinline__ void tma_load_bh(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                            int zh, uint64_t cache_hint, int bshd_h) {
+  if (bshd_h == 0) {
+    tma_load_3d(smem_dst, m, bar, c0, c1, zh, cache_hint);
+    return;
+  }
+  const int b = zh / bshd_h, h = zh - b * bshd_h;
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(h), "r"(b), "r"(smem_u32(bar)), "l"(cache_hint)
+      : "memory");
+}
 // 3-D tiled store shared -> global (bulk group).
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* smem_src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(

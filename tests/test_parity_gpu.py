@@ -456,3 +456,55 @@ def test_c5_full_size_sampled():
                               [16384], [16384], alpha, [b])
         err = relerr(f64(acc[0, hh])[rows], ref)
         assert err <= BF16_TOL, f"c5 key-split sum (h={hh}) rel err {err}"
+
+
+def _to_bshd(t):
+    return t.transpose(1, 2).contiguous()
+
+
+@pytest.mark.parametrize("d,dtype,det", [(64, "bf16", False), (64, "fp16", True), (128, "bf16", False),
+                                         (128, "bf16", True)])
+def test_layout_bshd_matches_bhsd(d, dtype, det):
+    """The paper's [Z, L, H, D] layout through strided TMA views: same arithmetic as the
+    [B, H, N, d] path, so O, dK, dV (and dQ in deterministic mode) are bitwise equal; padded rows 0."""
+    sa = _sa()
+    cfg = I.Config("bshd", B=3, H=3, N=320, d=d, lengths=[320, 129, 7], dtype=dtype, seed=31)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    alpha, b = 1 / math.sqrt(d), -math.log(320)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b)
+    dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b, deterministic=det)
+    qs, ks, vs, dos = (_to_bshd(t) for t in (q, k, v, do))
+    nan = lambda t: torch.full_like(t, float("nan"))  # noqa: E731
+    o2 = sa.sigattn_fwd(qs, ks, vs, nq, nk, alpha, b, out=nan(qs), layout="bshd")
+    dq2, dk2, dv2 = sa.sigattn_bwd(qs, ks, vs, dos, nq, nk, alpha, b, dq=nan(qs), dk=nan(ks), dv=nan(vs),
+                                   deterministic=det, layout="bshd")
+    o32 = sa.sigattn_fwd(qs, ks, vs, nq, nk, alpha, b, out_f32=True, layout="bshd")
+    torch.cuda.synchronize()
+    assert o2.shape == (3, 320, 3, d)
+    for name, a_, b_ in (("o", o, o2), ("dk", dk, dk2), ("dv", dv, dv2)):
+        assert torch.equal(a_, b_.transpose(1, 2)), f"{name}: bshd != bhsd"
+    if det:
+        assert torch.equal(dq, dq2.transpose(1, 2))
+    rdq = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, alpha, np.full(3, b))[0]
+    assert relerr(f64(dq2.transpose(1, 2)), rdq) <= BF16_TOL
+    assert relerr(f64(o32.transpose(1, 2)), f64(o)) <= 4e-3
+    for bb, n in enumerate(cfg.nq):
+        assert torch.all(o2[bb, n:] == 0) and torch.all(dq2[bb, n:] == 0)
+        assert torch.all(dk2[bb, n:] == 0) and torch.all(dv2[bb, n:] == 0)
+
+
+def test_layout_bshd_autograd():
+    """sigmoid_attention(..., layout='bshd') with a key_padding_mask: gradients through the library."""
+    sa = _sa()
+    cfg = I.Config("bshd_ag", B=2, H=2, N=256, d=64, lengths=[256, 100], seed=32)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    mask = torch.arange(256, device="cuda")[None, :] >= nk[:, None]
+    qq, kk, vv = (_to_bshd(t).requires_grad_(True) for t in (q, k, v))
+    o = sa.sigmoid_attention(qq, kk, vv, key_padding_mask=mask, layout="bshd")
+    o.backward(_to_bshd(do))
+    bias = np.full(2, -math.log(256))
+    ro = oracle.fwd(f64(q), f64(k), f64(v), cfg.nq, cfg.nk, 1 / 8, bias)
+    rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, 1 / 8, bias)
+    assert relerr(f64(o.transpose(1, 2)), ro) <= BF16_TOL
+    for got, ref in ((qq.grad, rdq), (kk.grad, rdk), (vv.grad, rdv)):
+        assert relerr(f64(got.transpose(1, 2)), ref) <= BF16_TOL
