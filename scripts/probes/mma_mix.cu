@@ -131,16 +131,17 @@ __global__ void __launch_bounds__(640, 1) probe(long long* out, int reps, int se
     long long t1 = clock64();
     if ((threadIdx.x & 31) == 0) { out[blockIdx.x] = t1 - t0; stop = 1; }
   } else if (warp < 16 && mode != 0) {
+    const uint32_t tcol = (mode & 4) ? 0u : 384u;   // mode 5: TMEM traffic on the MMAs' own columns
     const uint32_t lane_addr = ((warp & 3) * 32) << 16;
     uint32_t acc = 0;
     while (!stop) {
       if (mode & 1) {   // TMEM traffic on columns the MMAs do not use (384..447)
         float s[16];
-        sm100::tmem_ld16(tmem + lane_addr + 384 + (warp >> 2) * 16, s);
+        sm100::tmem_ld16(tmem + lane_addr + tcol + (warp >> 2) * 16, s);
         sm100::tmem_wait_ld_dep16(s);
         uint32_t pk[8];
         for (int i = 0; i < 8; ++i) pk[i] = __float_as_uint(s[2 * i] + s[2 * i + 1]);
-        sm100::tmem_st8(tmem + lane_addr + 384 + (warp >> 2) * 16, pk);
+        sm100::tmem_st8(tmem + lane_addr + tcol + 64 + (warp >> 2) * 16, pk);
         acc += pk[0];
       }
       if (mode & 2) {   // shared-memory stores, 32 B per thread per iteration
@@ -161,15 +162,15 @@ int main() {
   cudaMalloc(&d, 2048 * sizeof(long long));
   const int reps = 400, smem = 225 * 1024;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* modes[5] = {"alone", "+TMEM ld/st", "+st.shared", "+both", "random data"};
+  const char* modes[6] = {"alone", "+TMEM ld/st", "+st.shared", "+both", "random data", "+TMEM same cols"};
   printf("%-34s", "clk per MMA instruction");
-  for (int m = 0; m < 5; ++m) printf(" %12s", modes[m]);
+  for (int m = 0; m < 6; ++m) printf(" %12s", modes[m]);
   printf("   (ideal clk/instr)\n");
   const int N[kSeqs] = {64, 64, 128, 256, 64, 128, 64, 0, 0, 0, 0, 0};
   for (int seq = 0; seq < kSeqs; ++seq) {
     printf("%-34s", kNames[seq]);
-    for (int mode = 0; mode < 5; ++mode) {
-      probe<<<148, 640, smem>>>(d, reps, seq, mode == 4 ? 0 : mode, mode == 4);
+    for (int mode = 0; mode < 6; ++mode) {
+      probe<<<148, 640, smem>>>(d, reps, seq, mode == 4 ? 0 : (mode == 5 ? 5 : mode), mode == 4);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
       long long h;

@@ -508,3 +508,28 @@ def test_layout_bshd_autograd():
     assert relerr(f64(o.transpose(1, 2)), ro) <= BF16_TOL
     for got, ref in ((qq.grad, rdq), (kk.grad, rdk), (vv.grad, rdv)):
         assert relerr(f64(got.transpose(1, 2)), ref) <= BF16_TOL
+
+
+def test_encoder_layer_integration():
+    """§8f f4: the op inside Table 4's pre-LN encoder layer (hidden 768, 12 heads, d = 64), bf16,
+    jagged lengths, [B, N, H, d] projections read in place; forward and input/weight gradients
+    against the same layer composed in plain PyTorch fp32 (sigmoid attention written out)."""
+    from paper_2604_27124_b200.encoder import SigmoidEncoderLayer, reference_attention_fp32
+    torch.manual_seed(5)
+    layer = SigmoidEncoderLayer(dropout=0.0).cuda().to(torch.bfloat16)
+    B, N = 3, 384
+    lens = torch.tensor([384, 200, 57], dtype=torch.int32, device="cuda")
+    x = torch.randn(B, N, 768, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    y = layer(x, lens)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    layer_f = SigmoidEncoderLayer(dropout=0.0).cuda()   # fp32 copy of the same (bf16) weights
+    layer_f.load_state_dict({k_: v_.float() for k_, v_ in layer.state_dict().items()})
+    xr = x.detach().float().requires_grad_(True)
+    yr = reference_attention_fp32(layer_f, xr, lens)
+    yr.backward(gy.float())
+    assert relerr(f64(y - x), f64(yr - xr)) <= 3e-2
+    assert relerr(f64(x.grad), f64(xr.grad)) <= 3e-2
+    # weight gradient of the query projection flows through sigattn_bwd's dQ
+    wq = layer.q_proj.weight
+    assert relerr(f64(wq.grad), f64(layer_f.q_proj.weight.grad)) <= 5e-2
