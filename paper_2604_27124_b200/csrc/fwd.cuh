@@ -274,10 +274,13 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t d_s = tmem + (s_it % C::kSBuf) * 128;
       if (sm100::elect_one()) {
 #pragma unroll
+        // stage-base descriptors; a K step adds (offset >> 4) to the start-address field (no carry:
+        // every operand lies inside the CTA's shared window)
+        const uint64_t dq0 = sm100::make_sdesc_sw128(qa, 16, 1024), dk0 = sm100::make_sdesc_sw128(ka, 16, 1024);
+#pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
-          sm100::mma_ss(d_s, sm100::make_sdesc_sw128(qa + off, 16, 1024),
-                        sm100::make_sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
+          sm100::mma_ss(d_s, dq0 + (off >> 4), dk0 + (off >> 4), idesc_s, kk > 0);
         }
         sm100::mma_commit(&s_full[s_it % C::kSBuf]);
         sm100::mma_commit(&k_empty[st]);
@@ -303,12 +306,12 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t p_col = (si % C::kSBuf) * 128;
       if (sm100::elect_one()) {
         sm100::trace_event(args.trace, 1024 + si, 1536);
+        const uint64_t dv0 = sm100::make_sdesc_sw128(va, kTile * 128, 1024);
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk) {
           // P for keys [16kk, 16kk+16): pair warpgroup kk/4 packed its 64 keys at S cols [64 (kk/4), +32)
           const uint32_t a_col = p_col + (kk >> 2) * 64 + (kk & 3) * 8;
-          sm100::mma_ts(tmem + C::kColO + ob * D, tmem + a_col,
-                        sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
+          sm100::mma_ts(tmem + C::kColO + ob * D, tmem + a_col, dv0 + ((kk * 2048) >> 4), idesc_o,
                         (pc.j > 0 || kk > 0) ? 1u : 0u);
         }
         sm100::mma_commit(&v_empty[st]);
