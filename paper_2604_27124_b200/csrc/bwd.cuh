@@ -317,8 +317,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
-        sm100::tmem_cp_128x256b(tmem + C::kColK + kk * 8, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024));
-        sm100::tmem_cp_128x256b(tmem + C::kColV + kk * 8, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024));
+        sm100::tmem_cp_128x256b(tmem + C::kColK + kk * 8, sm100::sdesc_add(sm100::make_sdesc_sw128(ka, 16, 1024), kk * 32));
+        sm100::tmem_cp_128x256b(tmem + C::kColV + kk * 8, sm100::sdesc_add(sm100::make_sdesc_sw128(va, 16, 1024), kk * 32));
       }
     };
     // S^T_q = K Q_q^T and dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; A from TMEM)
@@ -328,22 +328,22 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
-        sm100::mma_ss(tmem + C::kColS + q * 64, sm100::make_sdesc_sw128(ka + kk * 32, 16, 1024),
-                      sm100::make_sdesc_sw128(qa + kk * 32, 16, 1024), idesc_s, kk > 0);
+        sm100::mma_ss(tmem + C::kColS + q * 64, sm100::sdesc_add(sm100::make_sdesc_sw128(ka, 16, 1024), kk * 32),
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(qa, 16, 1024), kk * 32), idesc_s, kk > 0);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
-        sm100::mma_ss(tmem + C::kColDP + q * 64, sm100::make_sdesc_sw128(va + kk * 32, 16, 1024),
-                      sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_s, kk > 0);
+        sm100::mma_ss(tmem + C::kColDP + q * 64, sm100::sdesc_add(sm100::make_sdesc_sw128(va, 16, 1024), kk * 32),
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(da, 16, 1024), kk * 32), idesc_s, kk > 0);
 #else
       (void)kvb;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
         sm100::mma_ts(tmem + C::kColS + q * 64, tmem + C::kColK + kk * 8,
-                      sm100::make_sdesc_sw128(qa + kk * 32, 16, 1024), idesc_s, kk > 0);
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(qa, 16, 1024), kk * 32), idesc_s, kk > 0);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
         sm100::mma_ts(tmem + C::kColDP + q * 64, tmem + C::kColV + kk * 8,
-                      sm100::make_sdesc_sw128(da + kk * 32, 16, 1024), idesc_s, kk > 0);
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(da, 16, 1024), kk * 32), idesc_s, kk > 0);
 #endif
       sm100::mma_commit(&s_full[q]);
     };
@@ -355,14 +355,14 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         // queries [64q + 16kk, +16): warpgroup kk packed them at S cols 64q + 16kk + [0, 8)
         const uint32_t a_col = q * 64 + kk * 16;
         sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + a_col,
-                      sm100::make_sdesc_sw128(da + kk * 2048, kTile * 128, 1024), idesc_acc,
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(da, kTile * 128, 1024), kk * 2048), idesc_acc,
                       (first && kk == 0) ? 0u : 1u);
       }
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const uint32_t a_col = q * 64 + kk * 16;
         sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + a_col,
-                      sm100::make_sdesc_sw128(qa + kk * 2048, kTile * 128, 1024), idesc_acc,
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(qa, kTile * 128, 1024), kk * 2048), idesc_acc,
                       (first && kk == 0) ? 0u : 1u);
       }
     };
@@ -404,8 +404,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         // dQ = dS K   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major, B = K MN-major)
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk)
-          sm100::mma_ss(tmem + C::kColDQ + qb * 64, sm100::make_sdesc_sw128(dsa + kk * 2048, kTile * 128, 1024),
-                        sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024), idesc_dq, kk > 0);
+          sm100::mma_ss(tmem + C::kColDQ + qb * 64, sm100::sdesc_add(sm100::make_sdesc_sw128(dsa, kTile * 128, 1024), kk * 2048),
+                        sm100::sdesc_add(sm100::make_sdesc_sw128(ka, kTile * 128, 1024), kk * 2048), idesc_dq, kk > 0);
         sm100::mma_commit(&ds_free[b2]);
         sm100::mma_commit(&dq_full[qb]);
         if (prev_last) sm100::mma_commit(&kv_empty[prev_kvb]);   // K/V smem slot free

@@ -43,7 +43,7 @@ struct Bwd128Cfg {
 };
 
 // kDQ = false: dK, dV only (deterministic backward, Alg. 3); see bwd.cuh.
-template <bool kBf16, bool kDQ = true, bool kDB = false>
+template <bool kBf16, bool kDQ = true, bool kDB = false, bool kBSHD = false>
 __global__ void __launch_bounds__(Bwd128Cfg::kThreads, 1)
 sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -118,8 +118,8 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sm100::mbar_arrive_expect_tx(kv_full, 2 * C::kKVBytes);
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-          sm100::tma_load_bh(smem + C::kKOff + s * (kTile * 128), &tmK, kv_full, s * 64, kt * kTile, zh, pol_kv, args.bshd ? args.H : 0);
-          sm100::tma_load_bh(smem + C::kVOff + s * (kTile * 128), &tmV, kv_full, s * 64, kt * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+          sm100::tma_load_bh(smem + C::kKOff + s * (kTile * 128), &tmK, kv_full, s * 64, kt * kTile, zh, pol_kv, kBSHD ? args.H : 0);
+          sm100::tma_load_bh(smem + C::kVOff + s * (kTile * 128), &tmV, kv_full, s * 64, kt * kTile, zh, pol_kv, kBSHD ? args.H : 0);
         }
       }
       __syncwarp();
@@ -131,9 +131,9 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             sm100::tma_load_bh(smem + C::kQOff + st * C::kQBytes + s * (C::kQT * 128), &tmQ, &qdo_full[st], s * 64,
-                               i * C::kQT, zh, pol_q, args.bshd ? args.H : 0);
+                               i * C::kQT, zh, pol_q, kBSHD ? args.H : 0);
             sm100::tma_load_bh(smem + C::kDOOff + st * C::kQBytes + s * (C::kQT * 128), &tmDO, &qdo_full[st],
-                               s * 64, i * C::kQT, zh, pol_q, args.bshd ? args.H : 0);
+                               s * 64, i * C::kQT, zh, pol_q, kBSHD ? args.H : 0);
           }
         }
         __syncwarp();
@@ -155,14 +155,14 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const uint32_t ko = (kk >> 2) * (kTile * 128) + (kk & 3) * 32, qo = (kk >> 2) * (C::kQT * 128) + (kk & 3) * 32;
-        sm100::mma_ss(tmem + C::kColS, sm100::make_sdesc_sw128(k_base + ko, 16, 1024),
-                      sm100::make_sdesc_sw128(qa + qo, 16, 1024), idesc_s, kk > 0);
+        sm100::mma_ss(tmem + C::kColS, sm100::sdesc_add(sm100::make_sdesc_sw128(k_base, 16, 1024), ko),
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(qa, 16, 1024), qo), idesc_s, kk > 0);
       }
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const uint32_t ko = (kk >> 2) * (kTile * 128) + (kk & 3) * 32, qo = (kk >> 2) * (C::kQT * 128) + (kk & 3) * 32;
-        sm100::mma_ss(tmem + C::kColDP, sm100::make_sdesc_sw128(v_base + ko, 16, 1024),
-                      sm100::make_sdesc_sw128(da + qo, 16, 1024), idesc_s, kk > 0);
+        sm100::mma_ss(tmem + C::kColDP, sm100::sdesc_add(sm100::make_sdesc_sw128(v_base, 16, 1024), ko),
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(da, 16, 1024), qo), idesc_s, kk > 0);
       }
       sm100::mma_commit(s_full);
     };
@@ -171,8 +171,8 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       // dQ^T = K^T dS^T: A = K read MN-major (M = d: 64-wide atoms at LBO = 16 KB), B = dS^T MN-major
 #pragma unroll
       for (int kk = 0; kk < kTile / 16; ++kk)
-        sm100::mma_ss(tmem + C::kColDQ, sm100::make_sdesc_sw128(k_base + kk * 2048, kTile * 128, 1024),
-                      sm100::make_sdesc_sw128(dsa + kk * 2048, 16, 1024), idesc_dq, kk > 0);
+        sm100::mma_ss(tmem + C::kColDQ, sm100::sdesc_add(sm100::make_sdesc_sw128(k_base, kTile * 128, 1024), kk * 2048),
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(dsa, 16, 1024), kk * 2048), idesc_dq, kk > 0);
     };
 
     uint32_t t = 0, item_c = 0;
@@ -198,12 +198,12 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 #pragma unroll
           for (int kk = 0; kk < C::kQT / 16; ++kk)   // dV += P^T dO  (queries 16kk: warpgroup kk's columns)
             sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + kk * 16,
-                          sm100::make_sdesc_sw128(da + kk * 2048, C::kQT * 128, 1024), idesc_acc,
+                          sm100::sdesc_add(sm100::make_sdesc_sw128(da, C::kQT * 128, 1024), kk * 2048), idesc_acc,
                           (i == 0 && kk == 0) ? 0u : 1u);
 #pragma unroll
           for (int kk = 0; kk < C::kQT / 16; ++kk)   // dK += dS^T Q
             sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + kk * 16,
-                          sm100::make_sdesc_sw128(qa + kk * 2048, C::kQT * 128, 1024), idesc_acc,
+                          sm100::sdesc_add(sm100::make_sdesc_sw128(qa, C::kQT * 128, 1024), kk * 2048), idesc_acc,
                           (i == 0 && kk == 0) ? 0u : 1u);
           sm100::mma_commit(&qdo_empty[st]);
           if (i == nqt - 1) sm100::mma_commit(acc_full);
@@ -325,7 +325,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       sm100::tc_fence_after();
       const int key = kt * kTile + (int)row;
       const bool key_valid = key < nk;
-      const size_t off = args.bshd ? row_off(1, args.H, args.Nk, D, b, h, key) : (zh * args.Nk + key) * D;
+      const size_t off = kBSHD ? row_off(1, args.H, args.Nk, D, b, h, key) : (zh * args.Nk + key) * D;
 #pragma unroll 1
       for (int which = 0; which < 2; ++which) {
         const uint32_t col0 = which == 0 ? C::kColDV : C::kColDK;
@@ -363,10 +363,10 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
   }
 
   if (warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
-    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, args.bshd);
-    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, args.bshd);
+    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0);
+    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0);
     if (args.dq_pad)   // dq_finalize_kernel covers the rows below
-      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, args.bshd);
+      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, kBSHD ? 1 : 0);
   }
 
   sm100::tc_fence_before();

@@ -192,14 +192,14 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
-            sm100::mma_ss(d_s, sm100::make_sdesc_sw128(qa + off, 16, 1024), sm100::make_sdesc_sw128(ka + off, 16, 1024),
+            sm100::mma_ss(d_s, sm100::sdesc_add(sm100::make_sdesc_sw128(qa, 16, 1024), off), sm100::sdesc_add(sm100::make_sdesc_sw128(ka, 16, 1024), off),
                           idesc_s, kk > 0);
           }
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
-            sm100::mma_ss(d_s + 64, sm100::make_sdesc_sw128(da + off, 16, 1024),
-                          sm100::make_sdesc_sw128(va + off, 16, 1024), idesc_s, kk > 0);
+            sm100::mma_ss(d_s + 64, sm100::sdesc_add(sm100::make_sdesc_sw128(da, 16, 1024), off),
+                          sm100::sdesc_add(sm100::make_sdesc_sw128(va, 16, 1024), off), idesc_s, kk > 0);
           }
           sm100::mma_commit(&s_full[u % C::kSBuf]);
           if (hh == 1) sm100::mma_commit(&v_empty[st]);   // last reader of V_j
@@ -223,7 +223,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
           for (int kk = 0; kk < 4; ++kk) {
             // keys [16 kk, +16) of the half: warpgroup kk/2 packed its 32 keys at columns [32 (kk/2), +16)
             const uint32_t a_col = ds_col + (kk >> 1) * 32 + (kk & 1) * 8;
-            sm100::mma_ts(tmem + C::kColDQ, tmem + a_col, sm100::make_sdesc_sw128(ka + kk * 2048, kTile * 128, 1024),
+            sm100::mma_ts(tmem + C::kColDQ, tmem + a_col, sm100::sdesc_add(sm100::make_sdesc_sw128(ka, kTile * 128, 1024), kk * 2048),
                           idesc_dq, (ul > 0 || kk > 0) ? 1u : 0u);
           }
           if (hh == 1) sm100::mma_commit(&k_empty[st]);   // last reader of K_j

@@ -180,8 +180,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * (kTile * 128) + (kk & 3) * 32;
-            sm100::mma_ss(tmem + x * 128, sm100::make_sdesc_sw128(qa + off, 16, 1024),
-                          sm100::make_sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
+            sm100::mma_ss(tmem + x * 128, sm100::sdesc_add(sm100::make_sdesc_sw128(qa, 16, 1024), off),
+                          sm100::sdesc_add(sm100::make_sdesc_sw128(ka, 16, 1024), off), idesc_s, kk > 0);
           }
           sm100::mma_commit(&s_full[x]);
           if (x == ntq - 1) sm100::mma_commit(&k_empty[st]);
@@ -203,7 +203,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             const uint32_t a_col = C::kSepP ? C::kColP + x * 64 + (kk >> 2) * 32 + (kk & 3) * 8
                                             : x * 128 + (kk >> 2) * 64 + (kk & 3) * 8;
             sm100::mma_ts(tmem + C::kColO + x * D, tmem + a_col,
-                          sm100::make_sdesc_sw128(va + kk * 2048, kTile * 128, 1024), idesc_o,
+                          sm100::sdesc_add(sm100::make_sdesc_sw128(va, kTile * 128, 1024), kk * 2048), idesc_o,
                           (j > 0 || kk > 0) ? 1u : 0u);
           }
           if (x == ntq - 1) sm100::mma_commit(&v_empty[st]);

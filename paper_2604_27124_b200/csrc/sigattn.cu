@@ -281,7 +281,7 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   a.dbias = p->dbias;
   a.trace = g_trace;
   a.bshd = layout_bshd(p) ? 1 : 0;
-  auto kern = sigattn_bwd128_kernel<kBf16, kDQ, kDB>;
+  auto kern = layout_bshd(p) ? sigattn_bwd128_kernel<kBf16, kDQ, kDB, true> : sigattn_bwd128_kernel<kBf16, kDQ, kDB, false>;
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);

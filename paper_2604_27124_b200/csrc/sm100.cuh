@@ -278,6 +278,13 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t smem_addr, uint32_
   return d;
 }
 
+// Descriptor of the same matrix moved by byte_off (a K step inside a stage): only the 14-bit
+// start-address field changes, and it cannot carry for operands inside the CTA's shared window, so
+// the stage-base descriptor is built once and each MMA pays one 32-bit add.
+__device__ __forceinline__ uint64_t sdesc_add(uint64_t d, uint32_t byte_off) {
+  return (d & 0xFFFFFFFF00000000ull) | (uint32_t)((uint32_t)d + (byte_off >> 4));
+}
+
 // ------------------------------------------------------------------ tcgen05: TMEM <-> registers
 // 32x32b shape: thread t of warp w reads lane (32*(w%4) + t), N consecutive 32-bit columns.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
