@@ -510,7 +510,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       for (int i = 0; i < nqt; ++i, ++t) {
 #pragma unroll
         for (int qh = 0; qh < 2; ++qh) {
-          sm100::mbar_wait(&s_full[qh], t & 1);
+          SIGATTN_COMPUTE_WAIT(&s_full[qh], t & 1);
 #define BWD_TR(e) if (lane == 0 && t >= 40 && t < 48) sm100::trace_event(args.trace, 4 * 512 + (warp * 8 + (t - 40)) * 8 + (e), 6 * 512)
           BWD_TR(qh == 0 ? 0 : 3);
           sm100::tc_fence_after();

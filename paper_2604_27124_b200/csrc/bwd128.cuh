@@ -256,7 +256,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       float db_acc = 0.f;
       for (int i = 0; i < nqt; ++i, ++t) {
-        sm100::mbar_wait(s_full, t & 1);
+        SIGATTN_COMPUTE_WAIT(s_full, t & 1);
         if (kDQ) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
         float s[16], dp[16];

@@ -296,7 +296,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     issue_s();
     for (uint32_t si = 0; pc.it < n_items; ++si) {
       issue_s();
-      sm100::mbar_wait_backoff(&p_full[si % C::kSBuf], (si / C::kSBuf) & 1);
+      SIGATTN_FWD_MMA_WAIT(&p_full[si % C::kSBuf], (si / C::kSBuf) & 1);
       const uint32_t ob = pc.c % C::kOBufs;
       if (pc.j == 0) sm100::mbar_wait(&o_empty[ob], ((pc.c / C::kOBufs) & 1) ^ 1);   // epilogue drained this O
       const uint32_t st = si % C::kStages;
@@ -347,7 +347,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         const uint32_t si = s_it + j;
         if ((si & 1) != pair) continue;          // the other warpgroup pair takes this key tile
         if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 3072 + si, 3584);
-        sm100::mbar_wait(&s_full[si % C::kSBuf], (si / C::kSBuf) & 1);
+        SIGATTN_COMPUTE_WAIT(&s_full[si % C::kSBuf], (si / C::kSBuf) & 1);
         if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 2048 + si, 2560);
         sm100::tc_fence_after();
 #pragma unroll

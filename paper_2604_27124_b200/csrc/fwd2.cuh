@@ -191,7 +191,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
       // O_x += P_x(j) V_j; the last PV of key tile j releases V_j
       auto issue_pv = [&](int x, int j) {
         const uint32_t kvi = kv_it + j, st = kvi % C::kStages;
-        sm100::mbar_wait_backoff(&p_full[x], xs[x] & 1);
+        SIGATTN_FWD_MMA_WAIT(&p_full[x], xs[x] & 1);
         if (j == 0) sm100::mbar_wait(&o_empty[x], (xo[x] & 1) ^ 1);   // epilogue drained O_x
         if (x == 0) sm100::mbar_wait(&v_full[st], (kvi / C::kStages) & 1);
         sm100::tc_fence_after();
@@ -260,7 +260,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
       const float b2 = bias * kLog2e;
       const bool row_valid = qt * kTile + (int)row < nq;
       for (int j = 0; j < nkt; ++j, ++xs) {
-        sm100::mbar_wait(&s_full[x], xs & 1);
+        SIGATTN_COMPUTE_WAIT(&s_full[x], xs & 1);
         sm100::tc_fence_after();
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {

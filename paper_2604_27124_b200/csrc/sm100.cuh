@@ -85,6 +85,20 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
       : "memory");
   return ok != 0;
 }
+// A lost mbarrier phase traps (the launch fails) instead of hanging the GPU.  The message costs a
+// printf call frame in every waiting role (measured: 6% of the backward), so it is opt-in.
+#ifndef SIGATTN_WATCHDOG_VERBOSE
+#define SIGATTN_WATCHDOG_VERBOSE 0
+#endif
+__device__ __forceinline__ void watchdog_report(uint64_t* bar, uint32_t parity) {
+#if SIGATTN_WATCHDOG_VERBOSE
+  printf("sigattn watchdog: block %d thread %d stuck on mbarrier %p parity %u\n", blockIdx.x, threadIdx.x, bar,
+         parity);
+#else
+  (void)bar;
+  (void)parity;
+#endif
+}
 template <bool kSleep>
 __device__ __forceinline__ void mbar_wait_impl(uint64_t* bar, uint32_t parity) {
   auto try_once = [&]() { return kSleep ? mbar_try_wait_sleep(bar, parity) : mbar_try_wait(bar, parity); };
@@ -94,8 +108,7 @@ __device__ __forceinline__ void mbar_wait_impl(uint64_t* bar, uint32_t parity) {
   uint32_t n = 0;
   while (!try_once()) {
     if ((++n & 1023u) == 0 && clock64() - t0 > (1ll << 35)) {  // ~17 s: a lost phase, not a slow kernel
-      printf("sigattn watchdog: block %d thread %d stuck on mbarrier %p parity %u\n", blockIdx.x, threadIdx.x,
-             bar, parity);
+      watchdog_report(bar, parity);
       __trap();
     }
   }
@@ -108,6 +121,26 @@ __device__ __forceinline__ void mbar_wait_impl(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_impl<false>(bar, parity); }
 // Same, sleeping in hardware between polls (for waits that are long and not latency critical).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) { mbar_wait_impl<true>(bar, parity); }
+// Waits of the sigmoid / compute warps for their next S tile.  SIGATTN_COMPUTE_SLEEP=1: try_wait
+// with a suspend-time hint (the warp sleeps in hardware instead of re-issuing try_wait), leaving the
+// issue slots of its sub-partition to the MMA warp.
+#ifndef SIGATTN_COMPUTE_SLEEP
+#define SIGATTN_COMPUTE_SLEEP 0
+#endif
+#if SIGATTN_COMPUTE_SLEEP
+#define SIGATTN_COMPUTE_WAIT(b, p) sm100::mbar_wait_sleep(b, p)
+#else
+#define SIGATTN_COMPUTE_WAIT(b, p) sm100::mbar_wait(b, p)
+#endif
+// The forward MMA warp's wait for P (SIGATTN_FWD_MMA_SPIN=1: spin instead of the nanosleep back-off).
+#ifndef SIGATTN_FWD_MMA_SPIN
+#define SIGATTN_FWD_MMA_SPIN 0
+#endif
+#if SIGATTN_FWD_MMA_SPIN
+#define SIGATTN_FWD_MMA_WAIT(b, p) sm100::mbar_wait(b, p)
+#else
+#define SIGATTN_FWD_MMA_WAIT(b, p) sm100::mbar_wait_backoff(b, p)
+#endif
 // Poll with a short nanosleep back-off: ~100-200 cycles of wake-up latency, few issue slots.
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
@@ -120,8 +153,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
     if (mbar_try_wait(bar, parity)) return;
 #if SIGATTN_WATCHDOG
     if ((++n & 1023u) == 0 && clock64() - t0 > (1ll << 35)) {
-      printf("sigattn watchdog: block %d thread %d stuck on mbarrier %p parity %u\n", blockIdx.x, threadIdx.x,
-             bar, parity);
+      watchdog_report(bar, parity);
       __trap();
     }
 #endif
