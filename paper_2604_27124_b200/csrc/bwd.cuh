@@ -159,18 +159,25 @@ struct TileIter {
 // s_taddr: TMEM address the 16 scores were loaded from (still intact: each warp packs P / dS over its
 // own columns only after this call).  SIGATTN_BWD_SPEC: the tier-4 sigma is evaluated before the warp
 // vote; on a failed vote the scores are reloaded from s_taddr and the exact tiers run.
+// spec: speculate tier 4 (updated to whether this chunk took tier 4, so a warp stops speculating
+// while its logits keep failing the vote).
 template <bool kMask, bool kBf16, bool kSum = false>
 __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
                                           float a2, float b2, bool key_valid, int nvalid, uint32_t s_taddr,
-                                          float* dsum = nullptr) {
+                                          bool& spec, float* dsum = nullptr) {
 #if SIGATTN_BWD_SPEC
-  if (!sigma_row_spec4<16, kMask>(v, a2, b2, key_valid, nvalid)) {   // v: scores in, P out
-    sm100::tmem_ld16(s_taddr, v);
-    sm100::tmem_wait_ld_dep16(v);
-    sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid);
+  bool done = false;
+  if (spec) {
+    done = sigma_row_spec4<16, kMask>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
+    if (!done) {
+      sm100::tmem_ld16(s_taddr, v);
+      sm100::tmem_wait_ld_dep16(v);
+    }
   }
+  if (!done) spec = sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid) == 4;   // one inlined copy
 #else
   (void)s_taddr;
+  (void)spec;
   sigma_row<16, kMask, SIGATTN_BWD_EMU>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
 #endif
   float s0 = 0.f, s1 = 0.f;
@@ -507,6 +514,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       float db_acc = 0.f;
+      bool spec = true;   // speculate tier 4 while the last chunk took it
       for (int i = 0; i < nqt; ++i, ++t) {
 #pragma unroll
         for (int qh = 0; qh < 2; ++qh) {
@@ -531,8 +539,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           // rows of padded keys)
           const int ncol = nq - (i * kTile + qh * 64 + (int)w4 * 16);
           uint32_t pp[8], dd[8];
-          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, &db_acc);
-          else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, &db_acc);
+          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
+          else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
           BWD_TR(qh == 0 ? 1 : 4);
           // P^T / dS^T over the first half of this warp's own (already read) columns; the epilogue
           // warpgroup stages dS^T into shared memory for the dQ MMA

@@ -255,6 +255,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       float db_acc = 0.f;
+      bool spec = true;   // speculate tier 4 while the last chunk took it
       for (int i = 0; i < nqt; ++i, ++t) {
         SIGATTN_COMPUTE_WAIT(s_full, t & 1);
         if (kDQ) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
@@ -266,8 +267,8 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sm100::tmem_wait_ld_dep16(dp);
         const int ncol = nq - (i * C::kQT + (int)w4 * 16);
         uint32_t pp[8], dd[8];
-        if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, &db_acc);
-        else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, &db_acc);
+        if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
+        else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
         sm100::tmem_st8(tmem + lane_addr + s_col, pp);
         sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
         if constexpr (kDQ) {

@@ -259,6 +259,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
       const float b2 = bias * kLog2e;
       const bool row_valid = qt * kTile + (int)row < nq;
       const bool warp_rows_valid = __all_sync(0xffffffffu, row_valid);
+      bool spec = true;   // speculate tier 4 while the last chunk took it
       const int U = 2 * nkt;
       for (int ul = 0; ul < U; ++ul) {
         const uint32_t u = u_it + ul;
@@ -276,8 +277,8 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
           sm100::tmem_wait_ld_dep16(s);
           sm100::tmem_wait_ld_dep16(dp);
           uint32_t pp[8], dd[8];
-          if (warp_rows_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col);
-          else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, row_valid, row_valid ? ncol : 0, tmem + lane_addr + s_col);
+          if (warp_rows_valid && ncol >= 16) bwd_row16<false, kBf16>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec);
+          else bwd_row16<true, kBf16>(s, dp, pp, dd, a2, b2, row_valid, row_valid ? ncol : 0, tmem + lane_addr + s_col, spec);
           // packed dS over this warpgroup's own, already-read S columns: [32 gp + 8 ch, +8)
           sm100::tmem_st8(tmem + lane_addr + sb + gp * 32 + ch * 8, dd);
         }

@@ -106,12 +106,14 @@ __device__ __forceinline__ void sigmoid_row32(float (&v)[32], uint32_t (&pk)[16]
 // the exact tiers of sigma_row run.
 template <bool kMask, bool kBf16>
 __device__ __forceinline__ void sigmoid_chunk32(uint32_t taddr, float (&v)[32], uint32_t (&pk)[16], float a, float c,
-                                                bool row_valid, int nvalid) {
+                                                bool row_valid, int nvalid, bool& spec) {
 #if SIGATTN_FWD_SPEC
-  if (!sigma_row_spec4<32, kMask>(v, a, c, row_valid, nvalid)) {
-    sm100::tmem_ld32_sync(taddr, v);
-    sigma_row<32, kMask, 0>(v, a, c, row_valid, nvalid);
+  bool done = false;
+  if (spec) {
+    done = sigma_row_spec4<32, kMask>(v, a, c, row_valid, nvalid);
+    if (!done) sm100::tmem_ld32_sync(taddr, v);
   }
+  if (!done) spec = sigma_row<32, kMask, 0>(v, a, c, row_valid, nvalid) == 4;   // one inlined copy
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
     float p0 = v[e], p1 = v[e + 1];
@@ -123,6 +125,7 @@ __device__ __forceinline__ void sigmoid_chunk32(uint32_t taddr, float (&v)[32], 
   }
 #else
   (void)taddr;
+  (void)spec;
   sigmoid_row32<kMask, kBf16>(v, pk, a, c, row_valid, nvalid);
 #endif
 }
@@ -332,6 +335,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t row = quarter * 32 + lane;    // tile row = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
+    bool spec = true;                            // speculate tier 4 while the last chunk took it
     uint32_t s_it = 0, c = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
@@ -361,8 +365,8 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
           for (int e = 0; e < 16; ++e) pk[e] = __float_as_uint(r[2 * e]) ^ __float_as_uint(r[2 * e + 1]);
 #else
-          if (nvalid >= 32) sigmoid_chunk32<false, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid);
-          else sigmoid_chunk32<true, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid);
+          if (nvalid >= 32) sigmoid_chunk32<false, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
+          else sigmoid_chunk32<true, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
 #endif
           // P over the first half of this warpgroup's 64 columns (chunk 0's columns are already read)
           sm100::tmem_st16(tmem + lane_addr + (si % C::kSBuf) * 128 + gp * 64 + ch * 16, pk);

@@ -246,6 +246,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;
     const uint32_t lane_addr = (quarter * 32) << 16;
+    bool spec = true;   // speculate tier 4 while the last chunk took it
     uint32_t xs = 0, xo = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
@@ -278,8 +279,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
             else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
           } else {
-            if (nvalid >= 32) sigmoid_chunk32<false, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid);
-            else sigmoid_chunk32<true, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid);
+            if (nvalid >= 32) sigmoid_chunk32<false, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
+            else sigmoid_chunk32<true, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
           }
           if (C::kSepP) {
             if (ch == 0) {   // PV_x(j-1) has read the previous P_x

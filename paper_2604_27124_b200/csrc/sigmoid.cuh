@@ -157,6 +157,8 @@ __device__ __forceinline__ void sigma2_from_t(float t0, float t1, float& p0, flo
 }
 
 // Speculative form of the common case: N scores of one row -> N values of the <= -4 tier (in place),
+// (callers speculate only while the previous chunk of the warp took tier 4: when the bias is mild
+// -- b = -log n for short sequences -- the vote fails often and speculation would double the work)
 // evaluated BEFORE the warp vote, so the max/vote chain runs beside the MUFU work instead of in front
 // of it.  Returns the vote: true iff every valid logit of the warp's chunk is <= -4, i.e. the values
 // are the tier-4 sigma.  On false the caller must redo the chunk from its scores with sigma_row
@@ -190,8 +192,9 @@ __device__ __forceinline__ bool sigma_row_spec4(float (&v)[N], float a, float c,
 // arithmetic the valid outputs see, so results stay bitwise independent of pad content.
 // kEmuEvery > 0: in the fast path, element pairs with index % kEmuEvery == kEmuEvery / 2 take the
 // FMA-pipe exp2 (exp2_fma2) instead of MUFU ex2, off-loading the MUFU unit (16 ops/clk/SM).
+// Returns the tier taken (warp-uniform): 4 (all valid logits <= -4), 2 (<= -2) or 0 (exact range).
 template <int N, bool kMask = false, int kEmuEvery = 0>
-__device__ __forceinline__ void sigma_row(float (&v)[N], float a, float c, bool lane_valid = true, int nvalid = N) {
+__device__ __forceinline__ int sigma_row(float (&v)[N], float a, float c, bool lane_valid = true, int nvalid = N) {
   float m = -INFINITY;
 #pragma unroll
   for (int e = 0; e < N; e += 2) {
@@ -204,6 +207,7 @@ __device__ __forceinline__ void sigma_row(float (&v)[N], float a, float c, bool 
   if (SIGATTN_SIGMA_TIER4 && __all_sync(0xffffffffu, !lane_valid || m <= kFastT4)) {
 #pragma unroll
     for (int e = 0; e < N; e += 2) sigma2_fast4(v[e], v[e + 1], v[e], v[e + 1]);
+    return 4;
   } else if (__all_sync(0xffffffffu, !lane_valid || m <= kFastT)) {
 #pragma unroll
     for (int e = 0; e < N; e += 2) {
@@ -212,9 +216,11 @@ __device__ __forceinline__ void sigma_row(float (&v)[N], float a, float c, bool 
       else
         sigma2_fast(v[e], v[e + 1], v[e], v[e + 1]);
     }
+    return 2;
   } else {
 #pragma unroll
     for (int e = 0; e < N; e += 2) sigma2_from_t(v[e], v[e + 1], v[e], v[e + 1]);
+    return 0;
   }
 }
 
