@@ -276,7 +276,6 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t ka = k_base + st * C::kTileBytes;
       const uint32_t d_s = tmem + (s_it % C::kSBuf) * 128;
       if (sm100::elect_one()) {
-#pragma unroll
         // stage-base descriptors; a K step adds (offset >> 4) to the start-address field (no carry:
         // every operand lies inside the CTA's shared window)
         const uint64_t dq0 = sm100::make_sdesc_sw128(qa, 16, 1024), dk0 = sm100::make_sdesc_sw128(ka, 16, 1024);
