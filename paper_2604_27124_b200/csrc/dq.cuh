@@ -60,7 +60,7 @@ struct DqCfg {
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 };
 
-template <int D, bool kBf16, bool kOutF32>
+template <int D, bool kBf16, bool kOutF32, bool kBSHD = false>
 __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
 sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -133,9 +133,9 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 #pragma unroll
         for (int s = 0; s < C::kSub; ++s) {
           sm100::tma_load_bh(smem + C::kQOff + qb * C::kTileBytes + s * (kTile * 128), &tmQ, &q_full[qb], s * 64,
-                             qt * kTile, zh, pol_q, args.bshd ? args.H : 0);
+                             qt * kTile, zh, pol_q, kBSHD ? args.H : 0);
           sm100::tma_load_bh(smem + C::kDOOff + qb * C::kTileBytes + s * (kTile * 128), &tmDO, &q_full[qb],
-                             s * 64, qt * kTile, zh, pol_q, args.bshd ? args.H : 0);
+                             s * 64, qt * kTile, zh, pol_q, kBSHD ? args.H : 0);
         }
       }
       __syncwarp();
@@ -147,7 +147,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
             sm100::tma_load_bh(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
-                               j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+                               j * kTile, zh, pol_kv, kBSHD ? args.H : 0);
         }
         __syncwarp();
         sm100::mbar_wait_backoff(&v_empty[st], ph ^ 1);
@@ -156,7 +156,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 #pragma unroll
           for (int s = 0; s < C::kSub; ++s)
             sm100::tma_load_bh(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
-                               j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+                               j * kTile, zh, pol_kv, kBSHD ? args.H : 0);
         }
         __syncwarp();
       }
@@ -302,7 +302,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
       if (qrow < args.Nq) {
         const bool valid = qrow < nq;
         const float alpha = args.scale;
-        const size_t off = row_off(args.bshd, args.H, args.Nq, D, b, h, qrow) + g * kPart;
+        const size_t off = row_off(kBSHD ? 1 : 0, args.H, args.Nq, D, b, h, qrow) + g * kPart;
         if constexpr (kOutF32) {
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.dq) + off);
 #pragma unroll
@@ -329,7 +329,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill)   // padded dQ rows beyond the last valid tile
     pad_fill_warp(args.dq, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
-                  kTile, lane, args.bshd);
+                  kTile, lane, kBSHD ? 1 : 0);
 
   sm100::tc_fence_before();
   __syncthreads();

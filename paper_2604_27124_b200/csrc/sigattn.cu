@@ -333,7 +333,7 @@ sigattn_status launch_dq(const sigattn_params* p, const void* q, const void* k, 
   a.dq = dq;
   a.bshd = layout_bshd(p) ? 1 : 0;
   using C = DqCfg<D>;
-  auto kern = sigattn_dq_kernel<D, kBf16, kF32>;
+  auto kern = layout_bshd(p) ? sigattn_dq_kernel<D, kBf16, kF32, true> : sigattn_dq_kernel<D, kBf16, kF32, false>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
