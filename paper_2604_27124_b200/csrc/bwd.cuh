@@ -156,15 +156,15 @@ struct TileIter {
 // 16 query columns of one key row: P^T and dS^T = P^T (1 - P^T) dP^T, packed to 16 bits.
 // kMask: columns e >= nvalid (padded queries) give P = dS = 0 (nvalid = 0 for a padded key row).
 // kSum: also accumulate the fp32 dS values into *dsum (learnable-bias gradient).
+// 16 query columns of one key row, step 1: scores -> P^T (fp32, in place).
 // s_taddr: TMEM address the 16 scores were loaded from (still intact: each warp packs P / dS over its
 // own columns only after this call).  SIGATTN_BWD_SPEC: the tier-4 sigma is evaluated before the warp
-// vote; on a failed vote the scores are reloaded from s_taddr and the exact tiers run.
-// spec: speculate tier 4 (updated to whether this chunk took tier 4, so a warp stops speculating
-// while its logits keep failing the vote).
-template <bool kMask, bool kBf16, bool kSum = false>
-__device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
-                                          float a2, float b2, bool key_valid, int nvalid, uint32_t s_taddr,
-                                          bool& spec, float* dsum = nullptr) {
+// vote; on a failed vote the scores are reloaded from s_taddr and the exact tiers run.  spec:
+// speculate tier 4 (updated to whether this chunk took tier 4, so a warp stops speculating while its
+// logits keep failing the vote).
+template <bool kMask>
+__device__ __forceinline__ void bwd_sigma16(float (&v)[16], float a2, float b2, bool key_valid, int nvalid,
+                                            uint32_t s_taddr, bool& spec) {
 #if SIGATTN_BWD_SPEC
   bool done = false;
   if (spec) {
@@ -180,6 +180,14 @@ __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16],
   (void)spec;
   sigma_row<16, kMask, SIGATTN_BWD_EMU>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
 #endif
+}
+
+// Step 2: dS^T = P^T (1 - P^T) dP^T, both packed to 16 bits.  kMask: columns e >= nvalid (padded
+// queries) give P = dS = 0 (nvalid = 0 for a padded key row).  kSum: also accumulate the fp32 dS
+// values into *dsum (learnable-bias gradient).
+template <bool kMask, bool kBf16, bool kSum = false>
+__device__ __forceinline__ void bwd_ds16(const float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8],
+                                         uint32_t (&dd)[8], int nvalid, float* dsum = nullptr) {
   float s0 = 0.f, s1 = 0.f;
 #pragma unroll
   for (int e = 0; e < 16; e += 2) {
@@ -197,6 +205,15 @@ __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16],
     dd[e >> 1] = sm100::pack2<kBf16>(d0, d1);
   }
   if constexpr (kSum) *dsum += s0 + s1;
+}
+
+// Both steps on 16 query columns of one key row (scores and dP^T already loaded).
+template <bool kMask, bool kBf16, bool kSum = false>
+__device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
+                                          float a2, float b2, bool key_valid, int nvalid, uint32_t s_taddr,
+                                          bool& spec, float* dsum = nullptr) {
+  bwd_sigma16<kMask>(v, a2, b2, key_valid, nvalid, s_taddr, spec);
+  bwd_ds16<kMask, kBf16, kSum>(v, dp, pp, dd, nvalid, dsum);
 }
 
 // Adds a warp's per-lane partial sums of dS into dbias[b] (one atomic per warp).

@@ -34,7 +34,7 @@ struct Bwd128Cfg {
   static constexpr int kDSOff = kDOOff + kQStages * kQBytes;
   static constexpr int kDSBytes = kTile * 128;               // [128 keys][64 q] 16-bit = 16 KB
   static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
-  static constexpr int kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 1;
+  static constexpr int kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kWarpEpi = 16, kWarpTMA = 20, kWarpMMA = 21, kWarpAlloc = 22, kWarpFill = 23;
   static constexpr int kThreads = 768;
@@ -64,6 +64,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
   uint64_t* dq_empty = dq_full + 1;
   uint64_t* acc_full = dq_empty + 1;
   uint64_t* acc_empty = acc_full + 1;
+  uint64_t* dp_full = acc_empty + 1;              // dP^T landed (S^T lands first: s_full)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -77,6 +78,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       sm100::mbar_init(&qdo_empty[i], 1);
     }
     sm100::mbar_init(s_full, 1);
+    sm100::mbar_init(dp_full, 1);
     sm100::mbar_init(p_full, 16);
     sm100::mbar_init(&ds_free[0], 1);
     sm100::mbar_init(&ds_free[1], 1);
@@ -160,11 +162,12 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       }
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
+        if (kk == 0) sm100::mma_commit(s_full);   // the compute warps start sigma while dP^T is computed
         const uint32_t ko = (kk >> 2) * (kTile * 128) + (kk & 3) * 32, qo = (kk >> 2) * (C::kQT * 128) + (kk & 3) * 32;
         sm100::mma_ss(tmem + C::kColDP, sm100::sdesc_add(sm100::make_sdesc_sw128(v_base, 16, 1024), ko),
                       sm100::sdesc_add(sm100::make_sdesc_sw128(da, 16, 1024), qo), idesc_s, kk > 0);
       }
-      sm100::mma_commit(s_full);
+      sm100::mma_commit(dp_full);
     };
     auto mma_dq = [&](uint32_t buf) {
       const uint32_t dsa = ds_base + buf * C::kDSBytes;
@@ -262,13 +265,20 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sm100::tc_fence_after();
         float s[16], dp[16];
         sm100::tmem_ld16(tmem + lane_addr + s_col, s);
-        sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
         sm100::tmem_wait_ld_dep16(s);
-        sm100::tmem_wait_ld_dep16(dp);
         const int ncol = nq - (i * C::kQT + (int)w4 * 16);
+        const bool full = warp_keys_valid && ncol >= 16;
+        const int nv = full ? 16 : (key_valid ? ncol : 0);
+        if (full) bwd_sigma16<false>(s, a2, b2, true, 16, tmem + lane_addr + s_col, spec);
+        else bwd_sigma16<true>(s, a2, b2, key_valid, nv, tmem + lane_addr + s_col, spec);
+        // dP^T lands after S^T: sigma above overlaps the dP^T MMAs
+        SIGATTN_COMPUTE_WAIT(dp_full, t & 1);
+        sm100::tc_fence_after();
+        sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
+        sm100::tmem_wait_ld_dep16(dp);
         uint32_t pp[8], dd[8];
-        if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
-        else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
+        if (full) bwd_ds16<false, kBf16, kDB>(s, dp, pp, dd, 16, &db_acc);
+        else bwd_ds16<true, kBf16, kDB>(s, dp, pp, dd, nv, &db_acc);
         sm100::tmem_st8(tmem + lane_addr + s_col, pp);
         sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
         if constexpr (kDQ) {
