@@ -33,7 +33,9 @@ struct Bwd128Cfg {
   static constexpr int kDOOff = kQOff + kQStages * kQBytes;
   static constexpr int kDSOff = kDOOff + kQStages * kQBytes;
   static constexpr int kDSBytes = kTile * 128;               // [128 keys][64 q] 16-bit = 16 KB
-  static constexpr int kBarOff = kDSOff + 2 * kDSBytes;
+  static constexpr int kDQOff = kDSOff + 2 * kDSBytes;       // fp32 dQ staging: 4 boxes [64 q][32 d] SW128
+  static constexpr int kDQBytes = kQT * D * 4;               // 32 KB
+  static constexpr int kBarOff = kDQOff + kDQBytes;
   static constexpr int kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kWarpEpi = 16, kWarpTMA = 20, kWarpMMA = 21, kWarpAlloc = 22, kWarpFill = 23;
@@ -47,7 +49,7 @@ template <bool kBf16, bool kDQ = true, bool kDB = false, bool kBSHD = false>
 __global__ void __launch_bounds__(Bwd128Cfg::kThreads, 1)
 sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                      const BwdArgs args) {
+                      const __grid_constant__ CUtensorMap tmDQ, const BwdArgs args) {
   using C = Bwd128Cfg;
   constexpr int D = C::D;
   extern __shared__ uint8_t smem_raw[];
@@ -299,6 +301,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     }
   } else if (warp < C::kWarpTMA) {
     // ===================== epilogue: dQ^T drain (lane = d index) + dK/dV =====================
+    constexpr uint32_t kEpiThread0 = 32 * C::kWarpEpi;
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // d index for dQ^T, key row for dK/dV
     const uint32_t lane_addr = (quarter * 32) << 16;
@@ -322,15 +325,31 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(dq_empty);
-        float* base = args.dq_acc + (zh * args.Nq + (size_t)i * C::kQT) * D + row;
-        const int nrow = nq - i * C::kQT;
+        // alpha dQ^T -> the fp32 staging tile [64 q][128 d] as four SW128 [64][32] boxes (thread = d
+        // index: every store of a warp hits 32 distinct banks), then one thread reduce-adds the boxes
+        // into the accumulator through the TMA (rows past Nq clipped; padded query rows add zeros).
+        uint8_t* dqs = smem + C::kDQOff;
+        if (threadIdx.x == kEpiThread0) sm100::bulk_wait_group_read<0>();   // previous tile's reduce read it
+        sm100::named_bar_sync(1, 128);
+        {
+          const uint32_t hh = row >> 5, j = row & 31;   // box, float within the 128-byte row
+          const uint32_t bbase = sm100::smem_u32(dqs) + hh * (C::kQT * 128) + (j & 3) * 4;
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4)
+          for (int c4 = 0; c4 < 4; ++c4)
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int q = c4 * 16 + e;
-            if (q < nrow) atomicAdd(base + (size_t)q * D, alpha * r[c4][e]);   // coalesced over d
-          }
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t q = c4 * 16 + e;
+              sm100::st_shared_f32(bbase + q * 128 + (((j >> 2) ^ (q & 7)) * 16), alpha * r[c4][e]);
+            }
+        }
+        sm100::fence_proxy_async_smem();
+        sm100::named_bar_sync(1, 128);
+        if (threadIdx.x == kEpiThread0) {
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh)
+            sm100::tma_reduce_add_3d(&tmDQ, dqs + hh * (C::kQT * 128), hh * 32, i * C::kQT, (int)zh);
+          sm100::bulk_commit_group();
+        }
       }
       sm100::mbar_wait_backoff(acc_full, item_c & 1);
       sm100::tc_fence_after();
@@ -380,6 +399,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, kBSHD ? 1 : 0);
   }
 
+  if (kDQ && threadIdx.x == 32 * C::kWarpEpi) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);

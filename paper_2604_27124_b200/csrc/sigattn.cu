@@ -262,6 +262,11 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   if ((st = make_tmap(&tk, k, dt, 2, 128, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
   if ((st = make_tmap(&tv, v, dt, 2, 128, p->Nk, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
   if ((st = make_tmap(&tdo, dout, dt, 2, 128, p->Nq, p->B, p->H, layout_bshd(p), Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
+  CUtensorMap tdq;   // fp32 dQ accumulator [B, H, Nq, 128], 32-column x 64-row boxes for the TMA reduce-add
+  std::memset(&tdq, 0, sizeof(tdq));
+  if (kDQ && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 128, p->Nq, p->B, p->H, false,
+                             Bwd128Cfg::kQT)) != SIGATTN_OK)
+    return st;
   BwdArgs a;
   a.items = items;
   a.n_items = n_items;
@@ -285,7 +290,7 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   prof_record(2, s);
-  kern<<<grid, Bwd128Cfg::kThreads, Bwd128Cfg::kSmemBytes, s>>>(tq, tk, tv, tdo, a);
+  kern<<<grid, Bwd128Cfg::kThreads, Bwd128Cfg::kSmemBytes, s>>>(tq, tk, tv, tdo, tdq, a);
   prof_record(3, s);
   count_launch();
   CUDA_TRY(cudaGetLastError());
