@@ -249,11 +249,12 @@ def test_sigmoid_slow_and_saturated_paths(bias, scale):
         assert err <= BF16_TOL, f"{name} rel err {err} (bias={bias}, scale={scale})"
 
 
-def test_cp_backward_partials_sum():
+@pytest.mark.parametrize("d", [64, 128])
+def test_cp_backward_partials_sum(d):
     """Key-split backward: per-block fp32 dQ partials (DQ_F32_PARTIAL) sum to dQ; dK/dV blocks are
     the unsplit dK/dV rows (keys are owned) -- the CP exchange of SURVEY 8e, simulated on one GPU."""
     sa = _sa()
-    cfg = I.Config("cpb", B=2, H=2, N=512, d=64, lengths=[512, 300], seed=16)
+    cfg = I.Config("cpb", B=2, H=2, N=512, d=d, lengths=[512, 300], seed=16)
     q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
     b = -math.log(512)
     G, blk = 4, 128
@@ -268,7 +269,7 @@ def test_cp_backward_partials_sum():
         dks.append(dk_r)
         dvs.append(dv_r)
     bias = np.full(2, b)
-    rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, 1 / 8, bias)
+    rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, 1 / math.sqrt(d), bias)
     assert relerr(f64(dq_sum), rdq) <= BF16_TOL
     assert relerr(f64(torch.cat(dks, 2)), rdk) <= BF16_TOL
     assert relerr(f64(torch.cat(dvs, 2)), rdv) <= BF16_TOL
