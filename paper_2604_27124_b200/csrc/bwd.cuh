@@ -43,6 +43,9 @@
 #else
 #define MMA_WAIT_P(b, p) sm100::mbar_wait_backoff(b, p)
 #endif
+#ifndef SIGATTN_BWD_MERGED_ISSUE
+#define SIGATTN_BWD_MERGED_ISSUE 0   // 1: one issue block per query half in the MMA warp
+#endif
 #ifndef SIGATTN_BWD_DQ_LATE
 #define SIGATTN_BWD_DQ_LATE 0
 #endif
@@ -443,6 +446,42 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1;
       const uint32_t st1 = (t + 1) % C::kQStages;
 #define MMA_TR(e) if (lane == 0 && t >= 40 && t < 48) sm100::trace_event(args.trace, 3328 + (t - 40) * 8 + (e), 4094)
+#if SIGATTN_BWD_MERGED_ISSUE
+      // one elected issue block per query half: every wait first, then dV/dK(t, h) and S/dP(t+1, h)
+      // back to back (fewer elect / fence / warp-sync sequences for the issue-starved MMA warp)
+#if !SIGATTN_DBG_MMAONLY
+      MMA_WAIT_P(&p_full[0], t & 1);
+      if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);   // epilogue read previous dV/dK
+#endif
+      if (nxt.valid) {
+        if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
+        sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
+#if !SIGATTN_DBG_MMAONLY
+        if (kDQ) sm100::mbar_wait(&ds_copied[0], t & 1);
+#endif
+      }
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        mma2(st, 0, cur.i == 0);
+        if (nxt.valid) {
+          if (!SIGATTN_BWD_SCORES_SS && nxt.i == 0) copy_kv(nxt.item_c & 1);
+          mma1(nxt.item_c & 1, st1, 0);
+        }
+      }
+      __syncwarp();
+#if !SIGATTN_DBG_MMAONLY
+      MMA_WAIT_P(&p_full[1], t & 1);
+      if (nxt.valid && kDQ) sm100::mbar_wait(&ds_copied[1], t & 1);
+#endif
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        mma2(st, 1, false);
+        sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
+        if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
+        if (nxt.valid) mma1(nxt.item_c & 1, st1, 1);
+      }
+      __syncwarp();
+#else
       MMA_TR(4);
       // long wait (a compute phase): poll with back-off so the MMA warp does not steal issue slots
 #if !SIGATTN_DBG_MMAONLY
@@ -498,6 +537,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 1);
         __syncwarp();
       }
+#endif
       MMA_TR(2);
       prev_kvb = kvb;
       prev_last = cur.i == cur.nqt - 1;
