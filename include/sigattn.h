@@ -132,6 +132,12 @@ void sigattn_set_profile_events(void* fwd_start, void* fwd_stop, void* bwd_start
  * kernels fill with clock64() pipeline timestamps (thread-local setting; NULL disables).  A no-op
  * in release builds.                                                                            */
 void sigattn_set_trace_buffer(void* device_buffer);
+/* Skip accounting: thread-local; when non-NULL, the attention kernels add
+ * the (query tile, key tile) pairs they actually execute to device uint64 counters:
+ * counters[0] forward (128 x 128 pairs), counters[1] backward key-tile pass (128 keys x its query
+ * tile: 128 rows for d = 64, 64 rows for d = 128), counters[2] deterministic dQ pass (128 x 128).
+ * The caller zeroes them; one atomic per work item.  NULL disables.                               */
+void sigattn_set_debug_counters(void* device_counters);
 
 const char* sigattn_last_error(void); /* thread-local message of the last failing call */
 const char* sigattn_version(void);

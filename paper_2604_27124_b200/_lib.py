@@ -25,7 +25,8 @@ STATUS_NAMES = {0: "SIGATTN_OK", 1: "SIGATTN_EINVAL", 2: "SIGATTN_EUNSUPPORTED",
 
 EXPORTED = ["sigattn_fwd", "sigattn_bwd", "sigattn_bwd_workspace_bytes", "sigattn_mask_to_seqlens",
             "sigattn_valid_flops", "sigattn_worklist_host", "sigattn_last_error", "sigattn_version",
-            "sigattn_launch_count", "sigattn_set_profile_events", "sigattn_set_trace_buffer"]
+            "sigattn_launch_count", "sigattn_set_profile_events", "sigattn_set_trace_buffer",
+            "sigattn_set_debug_counters"]
 
 
 class SigattnParams(ctypes.Structure):
@@ -78,6 +79,8 @@ def load():
     lib.sigattn_set_profile_events.restype = None
     lib.sigattn_set_trace_buffer.argtypes = [vp]
     lib.sigattn_set_trace_buffer.restype = None
+    lib.sigattn_set_debug_counters.argtypes = [vp]
+    lib.sigattn_set_debug_counters.restype = None
     lib.sigattn_last_error.restype = ctypes.c_char_p
     lib.sigattn_version.restype = ctypes.c_char_p
     _lib = lib

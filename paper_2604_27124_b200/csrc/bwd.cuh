@@ -101,6 +101,7 @@ struct BwdArgs {
   float* dbias;           // [B] fp32, zeroed at entry, += sum of dS (learnable bias gradient); or nullptr
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots (8 events x 512 tiles)
   int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
+  unsigned long long* counters;   // skip accounting (sigattn_set_debug_counters) or nullptr
 };
 
 template <int D>
@@ -478,6 +479,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         mma2(st, 1, false);
         sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
         if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
+        if (cur.i == 0 && args.counters) atomicAdd(args.counters + 1, (unsigned long long)cur.nqt);
         if (nxt.valid) mma1(nxt.item_c & 1, st1, 1);
       }
       __syncwarp();
@@ -526,6 +528,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         mma2(st, 1, false);
         sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
         if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
+        if (cur.i == 0 && args.counters) atomicAdd(args.counters + 1, (unsigned long long)cur.nqt);
       }
       __syncwarp();
       MMA_TR(1);

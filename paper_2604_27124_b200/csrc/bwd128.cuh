@@ -212,6 +212,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                           (i == 0 && kk == 0) ? 0u : 1u);
           sm100::mma_commit(&qdo_empty[st]);
           if (i == nqt - 1) sm100::mma_commit(acc_full);
+          if (i == 0 && args.counters) atomicAdd(args.counters + 1, (unsigned long long)nqt);
         }
         __syncwarp();
         const bool has_next_here = i + 1 < nqt;

@@ -34,6 +34,7 @@ struct DqArgs {
   int B, H, Nq, Nk;
   void* dq;               // bf16/fp16 [B,H,Nq,D], or fp32 when kOutF32 (context-parallel partial)
   int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
+  unsigned long long* counters;   // skip accounting (sigattn_set_debug_counters) or nullptr
 };
 
 template <int D>
@@ -174,6 +175,8 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int nkt = args.items[it].w;
       if (nkt <= 0) continue;
+      if (args.counters && sm100::elect_one()) atomicAdd(args.counters + 2, (unsigned long long)nkt);
+      __syncwarp();
       const uint32_t qb = c % C::kQBufs;
       sm100::mbar_wait(&q_full[qb], (c / C::kQBufs) & 1);
       const uint32_t qa = q_base + qb * C::kTileBytes, da = do_base + qb * C::kTileBytes;

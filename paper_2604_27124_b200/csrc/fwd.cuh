@@ -52,6 +52,7 @@ struct FwdArgs {
   int fill_pad;           // zero the O rows no tile epilogue writes (pad_fill_warp)
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots
   int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
+  unsigned long long* counters;   // skip accounting (sigattn_set_debug_counters) or nullptr
 };
 
 template <int D>
@@ -317,6 +318,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                         (pc.j > 0 || kk > 0) ? 1u : 0u);
         }
         sm100::mma_commit(&v_empty[st]);
+        if (pc.j == 0 && args.counters) atomicAdd(args.counters, (unsigned long long)pc.nkt);
         if (pc.j == pc.nkt - 1) {
           sm100::mma_commit(&q_empty[pc.c & 1]);
           sm100::mma_commit(&o_full[ob]);

@@ -168,6 +168,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
       const int nkt = item.w;
       if (nkt <= 0) continue;
       const int ntq = has_b(item.x, item.z) ? 2 : 1;
+      if (args.counters && sm100::elect_one()) atomicAdd(args.counters, (unsigned long long)(ntq * nkt));
+      __syncwarp();
       const uint32_t qb = c % C::kQBufs;
       sm100::mbar_wait(&q_full[qb], (c / C::kQBufs) & 1);
       // S_x(j) = Q_x K_j^T into slot x's buffer; the last S of key tile j releases K_j

@@ -37,6 +37,7 @@ thread_local std::string g_err;
 std::atomic<long long> g_launches{0};
 thread_local cudaEvent_t g_prof[4] = {nullptr, nullptr, nullptr, nullptr};
 thread_local long long* g_trace = nullptr;
+thread_local unsigned long long* g_counters = nullptr;
 
 void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
@@ -182,6 +183,7 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   a.o = o;
   a.fill_pad = (p->flags & SIGATTN_F_NO_ZERO_PAD_OUT) ? 0 : 1;
   a.trace = g_trace;
+  a.counters = g_counters;
   a.bshd = layout_bshd(p) ? 1 : 0;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   if constexpr (use_fwd2(D)) {
@@ -237,6 +239,7 @@ sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* 
   a.dq_pad = dq_pad;
   a.dbias = p->dbias;
   a.trace = g_trace;
+  a.counters = g_counters;
   a.bshd = layout_bshd(p) ? 1 : 0;
   using C = BwdCfg<D>;
   auto kern = layout_bshd(p) ? sigattn_bwd_kernel<D, kBf16, kDQ, kDB, true> : sigattn_bwd_kernel<D, kBf16, kDQ, kDB, false>;
@@ -285,6 +288,7 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   a.dq_pad = dq_pad;
   a.dbias = p->dbias;
   a.trace = g_trace;
+  a.counters = g_counters;
   a.bshd = layout_bshd(p) ? 1 : 0;
   auto kern = layout_bshd(p) ? sigattn_bwd128_kernel<kBf16, kDQ, kDB, true> : sigattn_bwd128_kernel<kBf16, kDQ, kDB, false>;
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
@@ -337,6 +341,7 @@ sigattn_status launch_dq(const sigattn_params* p, const void* q, const void* k, 
   a.Nk = p->Nk;
   a.dq = dq;
   a.bshd = layout_bshd(p) ? 1 : 0;
+  a.counters = g_counters;
   using C = DqCfg<D>;
   auto kern = layout_bshd(p) ? sigattn_dq_kernel<D, kBf16, kF32, true> : sigattn_dq_kernel<D, kBf16, kF32, false>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
@@ -389,6 +394,9 @@ const char* sigattn_last_error(void) { return g_err.c_str(); }
 int64_t sigattn_launch_count(void) { return g_launches.load(); }
 
 void sigattn_set_trace_buffer(void* device_buffer) { g_trace = reinterpret_cast<long long*>(device_buffer); }
+void sigattn_set_debug_counters(void* device_counters) {
+  g_counters = reinterpret_cast<unsigned long long*>(device_counters);
+}
 
 void sigattn_set_profile_events(void* fwd_start, void* fwd_stop, void* bwd_start, void* bwd_stop) {
   g_prof[0] = reinterpret_cast<cudaEvent_t>(fwd_start);

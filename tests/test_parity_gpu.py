@@ -534,3 +534,36 @@ def test_encoder_layer_integration():
     # weight gradient of the query projection flows through sigattn_bwd's dQ
     wq = layer.q_proj.weight
     assert relerr(f64(wq.grad), f64(layer_f.q_proj.weight.grad)) <= 5e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_skip_accounting_device_counters(d):
+    """Padded-tile skipping measured on the device (SURVEY 8(c) skip accounting): the
+    kernels execute exactly sum_b ceil(n_q/Bq) ceil(n_k/128) tile pairs per head -- none for n = 0,
+    none past a sequence's last valid tile -- in the forward, the backward and the deterministic dQ
+    pass (Bq = 128, except the d = 128 backward's 64-query tiles)."""
+    from paper_2604_27124_b200 import _lib
+    sa = _sa()
+    cfg = I.Config("skip", B=4, H=3, N=640, d=d, lengths=[640, 300, 1, 0], seed=41)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    lib.sigattn_set_debug_counters(cnt.data_ptr())
+    try:
+        sa.sigattn_fwd(q, k, v, nq, nk)
+        sa.sigattn_bwd(q, k, v, do, nq, nk)
+        sa.sigattn_bwd(q, k, v, do, nq, nk, deterministic=True)
+        torch.cuda.synchronize()
+    finally:
+        lib.sigattn_set_debug_counters(None)
+    c = lambda n, t: -(-n // t)  # noqa: E731
+    fwd = cfg.H * sum(c(n, 128) * c(n, 128) for n in cfg.nq)
+    bq = 128 if d == 64 else 64
+    bwd = cfg.H * sum(c(n, 128) * c(n, bq) for n in cfg.nq)
+    got = cnt.tolist()
+    assert got[0] == fwd, (got, fwd)
+    # fused backward + the deterministic run's key-tile pass both count into [1]
+    assert got[1] == 2 * bwd, (got, bwd)
+    assert got[2] == fwd, (got, fwd)
+    dense = cfg.H * cfg.B * c(640, 128) ** 2
+    assert got[0] < dense
