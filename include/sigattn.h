@@ -57,6 +57,13 @@ enum {
   SIGATTN_F_DQ_F32_PARTIAL = 1u << 2,  /* bwd: dq is float* fp32 alpha*dS K, not finalised
                                           (for the CP reduce-scatter)                        */
   SIGATTN_F_NO_ZERO_PAD_OUT = 1u << 3, /* caller does not need padded output rows zeroed     */
+  SIGATTN_F_SANITIZE_PAD = 1u << 5,    /* NaN-safe padding: before reading them, the library
+                                          zeroes IN PLACE the padded rows of q, k, v (and dout)
+                                          that share a 128-row tile with valid rows (rows
+                                          [n, ceil128(n)) of each sequence) -- the only padded
+                                          rows the kernels load.  Without it pad content must be
+                                          finite: a tensor core computes 0 * NaN = NaN (DESIGN R3).
+                                          The inputs are modified.                           */
   SIGATTN_F_LAYOUT_BSHD = 1u << 4      /* every tensor argument (q, k, v, o, dout, dq, dk, dv)
                                           is [B, N, H, d] -- the paper's [Z, L, H, D] layout
                                           (Alg. 1-3 Require lines) --

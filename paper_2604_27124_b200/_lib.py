@@ -19,6 +19,7 @@ SIGATTN_F_OUT_F32_PARTIAL = 1 << 1
 SIGATTN_F_DQ_F32_PARTIAL = 1 << 2
 SIGATTN_F_NO_ZERO_PAD_OUT = 1 << 3
 SIGATTN_F_LAYOUT_BSHD = 1 << 4
+SIGATTN_F_SANITIZE_PAD = 1 << 5
 
 STATUS_NAMES = {0: "SIGATTN_OK", 1: "SIGATTN_EINVAL", 2: "SIGATTN_EUNSUPPORTED", 3: "SIGATTN_ECUDA",
                 4: "SIGATTN_EWORKSPACE"}

@@ -106,7 +106,8 @@ def _stream_handle(device) -> int:
 
 def sigattn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens_q=None, seqlens_k=None,
                 scale: Optional[float] = None, bias: BiasArg = None, out: Optional[torch.Tensor] = None,
-                out_f32: bool = False, zero_pad_out: bool = True, layout: str = "bhsd") -> torch.Tensor:
+                out_f32: bool = False, zero_pad_out: bool = True, layout: str = "bhsd",
+                sanitize_pad: bool = False) -> torch.Tensor:
     """Forward (Alg. 1).  Returns O [B, H, Nq, d] ([B, Nq, H, d] for layout='bshd') in q.dtype
     (fp32 if out_f32: a CP partial)."""
     lib = _lib.load()
@@ -122,7 +123,7 @@ def sigattn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens_q=Non
     elif out.shape != oshape or out.dtype != odt or not out.is_contiguous():
         raise ValueError("sigattn: bad out tensor")
     flags = ((_lib.SIGATTN_F_OUT_F32_PARTIAL if out_f32 else 0) | (0 if zero_pad_out else _lib.SIGATTN_F_NO_ZERO_PAD_OUT)
-             | _layout_flag(layout))
+             | _layout_flag(layout) | (_lib.SIGATTN_F_SANITIZE_PAD if sanitize_pad else 0))
     p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags)
     _lib.check(lib.sigattn_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                _stream_handle(q.device)))
@@ -137,7 +138,8 @@ def bwd_workspace_bytes(B, H, Nq, Nk, d, dtype=torch.bfloat16) -> int:
 
 def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias: BiasArg = None,
                 dq=None, dk=None, dv=None, workspace: Optional[torch.Tensor] = None, dq_f32: bool = False,
-                deterministic: bool = False, dbias: Optional[torch.Tensor] = None, layout: str = "bhsd"):
+                deterministic: bool = False, dbias: Optional[torch.Tensor] = None, layout: str = "bhsd",
+                sanitize_pad: bool = False):
     """Backward (Alg. 2 + Alg. 3, fused).  Returns (dQ, dK, dV); dQ is fp32 if dq_f32 (CP partial).
 
     deterministic=True runs the paper's two passes instead (dK/dV key-tile-owned, dQ
@@ -160,7 +162,7 @@ def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias:
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
     flags = ((_lib.SIGATTN_F_DQ_F32_PARTIAL if dq_f32 else 0) | (_lib.SIGATTN_F_BWD_DETERMINISTIC if deterministic else 0)
-             | _layout_flag(layout))
+             | _layout_flag(layout) | (_lib.SIGATTN_F_SANITIZE_PAD if sanitize_pad else 0))
     if dbias is not None and (dbias.dtype != torch.float32 or dbias.numel() != B or not dbias.is_contiguous()
                               or not dbias.is_cuda):
         raise ValueError("sigattn: dbias must be a contiguous fp32 CUDA tensor with B entries")

@@ -164,6 +164,20 @@ __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, i
   }
 }
 
+// SIGATTN_F_SANITIZE_PAD: zero rows [n, min(ceil128(n), N)) of one (b, h) slab per CTA of a 16-bit
+// [B, H, N, D] (or [B, N, H, D]) tensor -- the padded rows that share a tile with valid rows.
+__global__ void sanitize_pad_kernel(void* t, int H, int N, int D, const int32_t* __restrict__ lens, int bshd) {
+  const int zh = blockIdx.x, b = zh / H, h = zh % H;
+  const int n = clamp_len(lens, b, N);
+  const int r1 = min((n + 127) / 128 * 128, N);
+  const int cpr = D * 2 / 16;   // 16-byte chunks per row
+  uint16_t* base = reinterpret_cast<uint16_t*>(t);
+  for (int i = threadIdx.x; i < (r1 - n) * cpr; i += blockDim.x) {
+    const int r = n + i / cpr, c = i % cpr;
+    reinterpret_cast<uint4*>(base + row_off(bshd, H, N, D, b, h, r))[c] = make_uint4(0, 0, 0, 0);
+  }
+}
+
 // Warp-cooperative dQ finalisation of rows [r0, r1) of one (b, h) slab:
 // dq[r] = r < n_q ? round(acc[r]) : 0.  (acc rows are read through L2, ld.global.cg.)
 template <bool kBf16>

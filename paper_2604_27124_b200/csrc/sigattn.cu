@@ -352,6 +352,15 @@ sigattn_status launch_dq(const sigattn_params* p, const void* q, const void* k, 
   return SIGATTN_OK;
 }
 
+// SIGATTN_F_SANITIZE_PAD: zero the padded rows inside each sequence's last valid tile, in place.
+sigattn_status sanitize_pad(const sigattn_params* p, const void* t, int N, const int32_t* lens, cudaStream_t s) {
+  if (!(p->flags & SIGATTN_F_SANITIZE_PAD) || !lens) return SIGATTN_OK;
+  sanitize_pad_kernel<<<p->B * p->H, 128, 0, s>>>(const_cast<void*>(t), p->H, N, p->d, lens, layout_bshd(p) ? 1 : 0);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Small device scratch for the forward work list, cached per (device, stream) so that calls on
@@ -455,6 +464,12 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
     return fail(SIGATTN_EINVAL, "tensor pointers must be 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  {
+    const int32_t* lk = p->seqlens_k;   // NULL: all keys valid
+    if ((st = sanitize_pad(p, q, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
+    if ((st = sanitize_pad(p, k, p->Nk, lk, s)) != SIGATTN_OK) return st;
+    if ((st = sanitize_pad(p, v, p->Nk, lk, s)) != SIGATTN_OK) return st;
+  }
   const bool f32 = (p->flags & SIGATTN_F_OUT_F32_PARTIAL) != 0;
   const int max_items = p->B * p->H * cdiv(p->Nq, 128);
   void* scratch = nullptr;
@@ -500,6 +515,13 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   if (workspace_bytes < need)
     return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  {
+    const int32_t* lk = p->seqlens_k;   // NULL: all keys valid
+    if ((st = sanitize_pad(p, q, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
+    if ((st = sanitize_pad(p, dout, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
+    if ((st = sanitize_pad(p, k, p->Nk, lk, s)) != SIGATTN_OK) return st;
+    if ((st = sanitize_pad(p, v, p->Nk, lk, s)) != SIGATTN_OK) return st;
+  }
   const bool dq_f32 = (p->flags & SIGATTN_F_DQ_F32_PARTIAL) != 0;
   if (dq_f32 && layout_bshd(p))
     return fail(SIGATTN_EUNSUPPORTED, "SIGATTN_F_DQ_F32_PARTIAL needs the [B, H, N, d] layout");

@@ -567,3 +567,31 @@ def test_skip_accounting_device_counters(d):
     assert got[2] == fwd, (got, fwd)
     dense = cfg.H * cfg.B * c(640, 128) ** 2
     assert got[0] < dense
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_sanitize_pad_nan_inputs(d):
+    """SIGATTN_F_SANITIZE_PAD: NaN in the padded rows of Q, K, V, dO (DESIGN R3: a tensor core
+    computes 0 * NaN = NaN) -- with the flag the outputs are finite, match the oracle on the valid
+    inputs and keep exact-zero padded rows; only rows [n, ceil128(n)) of the inputs are rewritten."""
+    sa = _sa()
+    cfg = I.Config("nanpad", B=3, H=2, N=384, d=d, lengths=[384, 200, 57], seed=43)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    ref = [f64(t) for t in (q, k, v, do)]           # oracle inputs: zero pad
+    for t in (q, k, v, do):
+        for bb, n in enumerate(cfg.nq):
+            t[bb, :, n:] = float("nan")
+    alpha, b = 1 / math.sqrt(d), -math.log(384)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b, sanitize_pad=True)
+    dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b, sanitize_pad=True)
+    torch.cuda.synchronize()
+    bias = np.full(cfg.B, b)
+    ro = oracle.fwd(ref[0], ref[1], ref[2], cfg.nq, cfg.nk, alpha, bias)
+    rdq, rdk, rdv = oracle.bwd(*ref, cfg.nq, cfg.nk, alpha, bias)
+    for name, got, r in (("o", o, ro), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+        assert torch.isfinite(got).all(), name
+        assert relerr(f64(got), r) <= BF16_TOL, name
+    for bb, n in enumerate(cfg.nq):
+        assert torch.all(o[bb, :, n:] == 0) and torch.all(dk[bb, :, n:] == 0)
+        t1 = min(-(-n // 128) * 128, 384)
+        assert torch.all(v[bb, :, n:t1] == 0) and torch.isnan(v[bb, :, t1:]).all()
