@@ -128,6 +128,19 @@ int64_t sigattn_valid_flops(int B, int H, int d, const int32_t* host_nq, const i
 int64_t sigattn_worklist_host(int kind, int B, int H, int Nq, int Nk, const int32_t* host_nq,
                               const int32_t* host_nk, int32_t* items, int64_t max_items);
 
+/* General (non-prefix) key_padding_mask [B, N] uint8 (1 = PAD) -> a stable compaction of every
+ * sequence: index [B, N] int32 (device) lists the valid positions in order, then the padded ones;
+ * seqlens [B] int32 (device) receives the valid counts.  Attention is equivariant under a joint
+ * permutation of a sequence's queries and keys (sigma is element-wise, Eq. 2), so
+ * permute_rows(gather) -> sigattn_fwd/bwd with seqlens -> permute_rows(scatter) is exact for any
+ * mask (self-attention, the same mask on queries and keys).                                      */
+sigattn_status sigattn_mask_to_index(const uint8_t* key_padding_mask, int B, int N, int32_t* index,
+                                     int32_t* seqlens, void* stream);
+/* Row permutation of a [B, H, N, d] 16-bit tensor (device, src != dst) by index [B, N]:
+ * scatter == 0: dst[b,h,r] = src[b,h,index[b,r]];  scatter == 1: dst[b,h,index[b,r]] = src[b,h,r].  */
+sigattn_status sigattn_permute_rows(const void* src, void* dst, const int32_t* index, int B, int H, int N,
+                                    int d, int scatter, void* stream);
+
 /* Instrumentation (bench / tests).  sigattn_launch_count(): number of kernels this library has
  * launched in this process so far (all entry points).  sigattn_set_profile_events(): thread-local;
  * when an event pair is non-NULL, the next sigattn_fwd / sigattn_bwd calls on this thread record

@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "SIGATTN_OK", 1: "SIGATTN_EINVAL", 2: "SIGATTN_EUNSUPPORTED",
 EXPORTED = ["sigattn_fwd", "sigattn_bwd", "sigattn_bwd_workspace_bytes", "sigattn_mask_to_seqlens",
             "sigattn_valid_flops", "sigattn_worklist_host", "sigattn_last_error", "sigattn_version",
             "sigattn_launch_count", "sigattn_set_profile_events", "sigattn_set_trace_buffer",
-            "sigattn_set_debug_counters"]
+            "sigattn_set_debug_counters", "sigattn_mask_to_index", "sigattn_permute_rows"]
 
 
 class SigattnParams(ctypes.Structure):
@@ -82,6 +82,11 @@ def load():
     lib.sigattn_set_trace_buffer.restype = None
     lib.sigattn_set_debug_counters.argtypes = [vp]
     lib.sigattn_set_debug_counters.restype = None
+    lib.sigattn_mask_to_index.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
+    lib.sigattn_mask_to_index.restype = ctypes.c_int
+    lib.sigattn_permute_rows.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, vp]
+    lib.sigattn_permute_rows.restype = ctypes.c_int
     lib.sigattn_last_error.restype = ctypes.c_char_p
     lib.sigattn_version.restype = ctypes.c_char_p
     _lib = lib

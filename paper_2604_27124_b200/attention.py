@@ -177,6 +177,18 @@ def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias:
     return dq, dk, dv
 
 
+def _mask_lens_and_flag(key_padding_mask: torch.Tensor):
+    """(seqlens [B] int32 on device, whether the mask is non-prefix) -- both from the library kernel."""
+    lib = _lib.load()
+    m = key_padding_mask.to(torch.uint8).contiguous()
+    B, N = m.shape
+    seqlens = torch.empty(B, dtype=torch.int32, device=m.device)
+    flag = torch.empty(1, dtype=torch.int32, device=m.device)
+    _lib.check(lib.sigattn_mask_to_seqlens(m.data_ptr(), B, N, seqlens.data_ptr(), flag.data_ptr(),
+                                           _stream_handle(m.device)))
+    return seqlens, int(flag.item()) != 0
+
+
 def sigattn_mask_to_seqlens(key_padding_mask: torch.Tensor, check_prefix: bool = True) -> torch.Tensor:
     """PyTorch key_padding_mask [B, N] (True = pad) -> int32 valid lengths, on device."""
     lib = _lib.load()
@@ -189,6 +201,46 @@ def sigattn_mask_to_seqlens(key_padding_mask: torch.Tensor, check_prefix: bool =
     if check_prefix and int(flag.item()) != 0:
         raise ValueError("sigattn: key_padding_mask is not a prefix mask (valid tokens after padding)")
     return seqlens
+
+
+def sigattn_mask_to_index(key_padding_mask: torch.Tensor):
+    """General key_padding_mask [B, N] (True = pad) -> (index [B, N] int32, seqlens [B] int32), on
+    device: index lists each sequence's valid positions in order, then its padded ones."""
+    lib = _lib.load()
+    m = key_padding_mask.to(torch.uint8).contiguous()
+    B, N = m.shape
+    index = torch.empty((B, N), dtype=torch.int32, device=m.device)
+    seqlens = torch.empty(B, dtype=torch.int32, device=m.device)
+    _lib.check(lib.sigattn_mask_to_index(m.data_ptr(), B, N, index.data_ptr(), seqlens.data_ptr(),
+                                         _stream_handle(m.device)))
+    return index, seqlens
+
+
+def sigattn_permute_rows(x: torch.Tensor, index: torch.Tensor, scatter: bool) -> torch.Tensor:
+    """[B, H, N, d] row gather (out[:, :, r] = x[:, :, index[r]]) or scatter (out[:, :, index[r]] = x[:, :, r])."""
+    lib = _lib.load()
+    if not x.is_contiguous() or x.dim() != 4:
+        raise ValueError("sigattn: permute_rows needs a contiguous [B, H, N, d] tensor")
+    B, H, N, d = x.shape
+    out = torch.empty_like(x)
+    _lib.check(lib.sigattn_permute_rows(x.data_ptr(), out.data_ptr(), index.data_ptr(), B, H, N, d,
+                                        1 if scatter else 0, _stream_handle(x.device)))
+    return out
+
+
+class _PermuteRows(torch.autograd.Function):
+    """Row permutation along N; its gradient is the inverse permutation (library kernels both ways)."""
+
+    @staticmethod
+    def forward(ctx, x, index, scatter):
+        ctx.save_for_backward(index)
+        ctx.scatter = scatter
+        return sigattn_permute_rows(x, index, scatter)
+
+    @staticmethod
+    def backward(ctx, g):
+        (index,) = ctx.saved_tensors
+        return sigattn_permute_rows(g.contiguous(), index, not ctx.scatter), None, None
 
 
 def valid_flops(B: int, H: int, d: int, nq, nk, forward: bool) -> int:
@@ -257,7 +309,17 @@ def sigmoid_attention(q, k, v, seqlens_q=None, seqlens_k=None, key_padding_mask=
     if key_padding_mask is not None:
         if seqlens_k is not None:
             raise ValueError("give seqlens or key_padding_mask, not both")
-        seqlens_k = sigattn_mask_to_seqlens(key_padding_mask)
+        lens, nonprefix = _mask_lens_and_flag(key_padding_mask)
+        if nonprefix:
+            # general mask: compact every sequence (stable), attend with prefix lengths, scatter back
+            # -- exact, the op is equivariant under a joint permutation of queries and keys (Eq. 2)
+            if layout != "bhsd" or q.shape[2] != k.shape[2] or seqlens_q is not None:
+                raise ValueError("sigattn: a non-prefix key_padding_mask needs self-attention in 'bhsd' layout")
+            index, lens = sigattn_mask_to_index(key_padding_mask)
+            qc, kc, vc = (_PermuteRows.apply(t.contiguous(), index, False) for t in (q, k, v))
+            oc = SigmoidAttentionFn.apply(qc, kc, vc, lens, lens, scale, bias, deterministic, layout)
+            return _PermuteRows.apply(oc, index, True)
+        seqlens_k = lens
         if seqlens_q is None and q.shape[ndim] == k.shape[ndim]:
             seqlens_q = seqlens_k
     B = q.shape[0]

@@ -230,6 +230,75 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, uint16_t* __re
                             threadIdx.x & 31, bshd ? (size_t)H * D : (size_t)D);
 }
 
+// General (non-prefix) key_padding_mask [B, N] (1 = pad) -> a stable compaction per sequence:
+// index[b, r] = position of the r-th valid token for r < n_b, then of the (r - n_b)-th padded one;
+// seqlens[b] = n_b.  One CTA of 1024 threads per sequence; chunks of 1024 positions scanned with
+// warp ballots.  Attention is equivariant under a joint permutation of the queries and keys of a
+// sequence, so compacting, attending with prefix lengths and scattering back is exact.
+__global__ void __launch_bounds__(1024) mask_to_index_kernel(const uint8_t* __restrict__ mask, int N,
+                                                             int32_t* __restrict__ index,
+                                                             int32_t* __restrict__ seqlens) {
+  const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ int s_warp[32];
+  __shared__ int s_total;
+  // pass 1: number of valid tokens
+  int valid = 0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) valid += mask[(size_t)b * N + i] == 0;
+  for (int o = 16; o > 0; o >>= 1) valid += __shfl_xor_sync(0xffffffffu, valid, o);
+  if (lane == 0) s_warp[warp] = valid;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_warp[w];
+    s_total = t;
+    seqlens[b] = t;
+  }
+  __syncthreads();
+  const int n = s_total;
+  int base_v = 0, base_p = 0;   // valid / padded tokens before this chunk
+  for (int c0 = 0; c0 < N; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const bool in = i < N;
+    const bool v = in && mask[(size_t)b * N + i] == 0;
+    const unsigned bv = __ballot_sync(0xffffffffu, v), bp = __ballot_sync(0xffffffffu, in && !v);
+    __syncthreads();
+    if (lane == 0) s_warp[warp] = __popc(bv) | (__popc(bp) << 16);
+    __syncthreads();
+    int pv = 0, pp = 0;
+    for (int w = 0; w < warp; ++w) {
+      pv += s_warp[w] & 0xffff;
+      pp += s_warp[w] >> 16;
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    if (v) index[(size_t)b * N + base_v + pv + __popc(bv & lt)] = i;
+    else if (in) index[(size_t)b * N + n + base_p + pp + __popc(bp & lt)] = i;
+    int tv = 0, tp = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      tv += s_warp[w] & 0xffff;
+      tp += s_warp[w] >> 16;
+    }
+    base_v += tv;
+    base_p += tp;
+  }
+}
+
+// Row gather / scatter of a [B, H, N, D] 16-bit tensor along N by index [B, N]:
+// scatter = 0: dst[b, h, r] = src[b, h, index[b, r]];  scatter = 1: dst[b, h, index[b, r]] = src[b, h, r].
+// Grid (B*H, ceil(N / 8)), 128 threads: 8 rows per CTA, 16-byte chunks.
+__global__ void permute_rows_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
+                                    const int32_t* __restrict__ index, int H, int N, int D, int scatter) {
+  const int zh = blockIdx.x, b = zh / H;
+  const int cpr = D / 8;
+  const size_t slab = (size_t)zh * N * D;
+  for (int i = threadIdx.x; i < 8 * cpr; i += blockDim.x) {
+    const int r = blockIdx.y * 8 + i / cpr, c = i % cpr;
+    if (r >= N) continue;
+    const int j = index[(size_t)b * N + r];
+    const int rs = scatter ? r : j, rd = scatter ? j : r;
+    reinterpret_cast<uint4*>(dst + slab + (size_t)rd * D)[c] = reinterpret_cast<const uint4*>(src + slab + (size_t)rs * D)[c];
+  }
+}
+
 // key_padding_mask [B, N] (1 = pad) -> seqlens[b] = number of valid tokens; flags non-prefix masks.
 __global__ void mask_to_seqlens_kernel(const uint8_t* __restrict__ mask, int N, int32_t* __restrict__ seqlens,
                                        int32_t* __restrict__ nonprefix) {

@@ -586,6 +586,32 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   return SIGATTN_OK;
 }
 
+sigattn_status sigattn_mask_to_index(const uint8_t* key_padding_mask, int B, int N, int32_t* index,
+                                     int32_t* seqlens, void* stream) {
+  if (!key_padding_mask || !index || !seqlens || B <= 0 || N <= 0 || N > 65535)
+    return fail(SIGATTN_EINVAL, "bad mask_to_index arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  mask_to_index_kernel<<<B, 1024, 0, s>>>(key_padding_mask, N, index, seqlens);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+sigattn_status sigattn_permute_rows(const void* src, void* dst, const int32_t* index, int B, int H, int N, int d,
+                                    int scatter, void* stream) {
+  if (!src || !dst || !index || src == dst || B <= 0 || H <= 0 || N <= 0 || (d != 64 && d != 128))
+    return fail(SIGATTN_EINVAL, "bad permute_rows arguments");
+  if (!aligned16(src) || !aligned16(dst)) return fail(SIGATTN_EINVAL, "tensor pointers must be 16-byte aligned");
+  if ((long long)B * H > 65535 * 1024ll) return fail(SIGATTN_EUNSUPPORTED, "B*H too large");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const dim3 grid(B * H, (N + 7) / 8);
+  permute_rows_kernel<<<grid, 128, 0, s>>>(reinterpret_cast<const uint16_t*>(src), reinterpret_cast<uint16_t*>(dst),
+                                           index, H, N, d, scatter);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
 sigattn_status sigattn_mask_to_seqlens(const uint8_t* key_padding_mask, int B, int N, int32_t* seqlens,
                                        int32_t* nonprefix_flag, void* stream) {
   if (!key_padding_mask || !seqlens || !nonprefix_flag || B <= 0 || N <= 0)
