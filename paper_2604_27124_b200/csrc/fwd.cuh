@@ -57,7 +57,10 @@ struct FwdArgs {
 
 template <int D>
 struct FwdCfg {
-  static constexpr int kStages = (D == 64) ? 4 : 2;
+#ifndef SIGATTN_FWD_STAGES
+#define SIGATTN_FWD_STAGES 4
+#endif
+  static constexpr int kStages = (D == 64) ? SIGATTN_FWD_STAGES : 2;
   static constexpr int kSub = D / 64;                       // 64-column (128 B) swizzle atoms per row
   static constexpr int kTileBytes = kTile * D * 2;          // one 128-row tile of Q, K or V
   static constexpr int kQOff = 0;                           // Q[2]
