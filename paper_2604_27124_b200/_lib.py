@@ -80,13 +80,18 @@ def load():
     lib.sigattn_set_profile_events.restype = None
     lib.sigattn_set_trace_buffer.argtypes = [vp]
     lib.sigattn_set_trace_buffer.restype = None
-    lib.sigattn_set_debug_counters.argtypes = [vp]
-    lib.sigattn_set_debug_counters.restype = None
-    lib.sigattn_mask_to_index.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
-    lib.sigattn_mask_to_index.restype = ctypes.c_int
-    lib.sigattn_permute_rows.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                         ctypes.c_int, vp]
-    lib.sigattn_permute_rows.restype = ctypes.c_int
+    # newer entry points: typed when present (an older experimental build loaded through $SIGATTN_LIB
+    # for an A/B may predate them; test_abi_cpu checks that the in-tree library exports every one)
+    if hasattr(lib, "sigattn_set_debug_counters"):
+        lib.sigattn_set_debug_counters.argtypes = [vp]
+        lib.sigattn_set_debug_counters.restype = None
+    if hasattr(lib, "sigattn_mask_to_index"):
+        lib.sigattn_mask_to_index.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        lib.sigattn_mask_to_index.restype = ctypes.c_int
+    if hasattr(lib, "sigattn_permute_rows"):
+        lib.sigattn_permute_rows.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int, vp]
+        lib.sigattn_permute_rows.restype = ctypes.c_int
     lib.sigattn_last_error.restype = ctypes.c_char_p
     lib.sigattn_version.restype = ctypes.c_char_p
     _lib = lib
