@@ -64,6 +64,9 @@
 #ifndef SIGATTN_BWD_SPEC
 #define SIGATTN_BWD_SPEC 1        // tier-4 sigma evaluated before the warp vote (sigma_row_spec4)
 #endif
+#ifndef SIGATTN_BWD64_SPEC
+#define SIGATTN_BWD64_SPEC false  // ... in the d = 64 fused backward: vote first measured 1.5-8% faster
+#endif
 #ifndef SIGATTN_BWD_EMU
 #define SIGATTN_BWD_EMU 0         // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
 #endif
@@ -166,9 +169,15 @@ struct TileIter {
 // vote; on a failed vote the scores are reloaded from s_taddr and the exact tiers run.  spec:
 // speculate tier 4 (updated to whether this chunk took tier 4, so a warp stops speculating while its
 // logits keep failing the vote).
-template <bool kMask>
+template <bool kMask, bool kSpec = true>
 __device__ __forceinline__ void bwd_sigma16(float (&v)[16], float a2, float b2, bool key_valid, int nvalid,
                                             uint32_t s_taddr, bool& spec) {
+  if constexpr (!kSpec) {   // vote first (measured better for the d = 64 fused backward)
+    (void)s_taddr;
+    (void)spec;
+    sigma_row<16, kMask, SIGATTN_BWD_EMU>(v, a2, b2, key_valid, nvalid);
+    return;
+  }
 #if SIGATTN_BWD_SPEC
   bool done = false;
   if (spec) {
@@ -212,11 +221,11 @@ __device__ __forceinline__ void bwd_ds16(const float (&v)[16], const float (&dp)
 }
 
 // Both steps on 16 query columns of one key row (scores and dP^T already loaded).
-template <bool kMask, bool kBf16, bool kSum = false>
+template <bool kMask, bool kBf16, bool kSum = false, bool kSpec = true>
 __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
                                           float a2, float b2, bool key_valid, int nvalid, uint32_t s_taddr,
                                           bool& spec, float* dsum = nullptr) {
-  bwd_sigma16<kMask>(v, a2, b2, key_valid, nvalid, s_taddr, spec);
+  bwd_sigma16<kMask, kSpec>(v, a2, b2, key_valid, nvalid, s_taddr, spec);
   bwd_ds16<kMask, kBf16, kSum>(v, dp, pp, dd, nvalid, dsum);
 }
 
@@ -599,8 +608,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           // rows of padded keys)
           const int ncol = nq - (i * kTile + qh * 64 + (int)w4 * 16);
           uint32_t pp[8], dd[8];
-          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
-          else bwd_row16<true, kBf16, kDB>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
+          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB, SIGATTN_BWD64_SPEC>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
+          else bwd_row16<true, kBf16, kDB, SIGATTN_BWD64_SPEC>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
           BWD_TR(qh == 0 ? 1 : 4);
           // P^T / dS^T over the first half of this warp's own (already read) columns; the epilogue
           // warpgroup stages dS^T into shared memory for the dQ MMA
