@@ -222,6 +222,7 @@ def main_ours(args):
     o = torch.empty_like(q)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     ws = torch.empty(sa.bwd_workspace_bytes(cfg.B, cfg.H, cfg.N, cfg.N, cfg.d), dtype=torch.uint8, device=dev)
+    fws = torch.empty(sa.fwd_workspace_bytes(cfg.B, cfg.H, cfg.N, cfg.N, cfg.d), dtype=torch.uint8, device=dev)
     if args.workload != "c3":
         args.no_e2e = True
         args.no_cpu_baseline = True
@@ -229,7 +230,7 @@ def main_ours(args):
     f_bwd = sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, False)
 
     def step():
-        sa.sigattn_fwd(q, k, v, nq, nk, alpha, bias, out=o)
+        sa.sigattn_fwd(q, k, v, nq, nk, alpha, bias, out=o, workspace=fws)
         sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, bias, dq=dq, dk=dk, dv=dv, workspace=ws)
 
     for _ in range(max(3, args.warmup)):
@@ -292,7 +293,7 @@ def main_ours(args):
             dq_, dk_, dv_ = (t_.to(dev, non_blocking=True) for t_ in (hq, hk, hv))
             ddo = hdo.to(dev, non_blocking=True)
             snq, snk = hnq.to(dev, non_blocking=True), hnk.to(dev, non_blocking=True)
-            oo = sa.sigattn_fwd(dq_, dk_, dv_, snq, snk, alpha, bias)
+            oo = sa.sigattn_fwd(dq_, dk_, dv_, snq, snk, alpha, bias, workspace=fws)
             g1, g2, g3 = sa.sigattn_bwd(dq_, dk_, dv_, ddo, snq, snk, alpha, bias, workspace=ws)
             ho.copy_(oo, non_blocking=True)
             hdq.copy_(g1, non_blocking=True)

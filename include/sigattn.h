@@ -21,7 +21,12 @@
  *     rows.  Pad CONTENT must be finite (a tensor core computes 0 * NaN = NaN); with finite pad
  *     the outputs are independent of it.
  *   - All calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy
- *     default stream).  No host synchronisation happens inside a call.  Calls are reentrant.
+ *     default stream).  No host synchronisation happens inside a call.  The library allocates no
+ *     device memory: every buffer, workspaces included, is the caller's.  Calls are reentrant
+ *     and may run concurrently from several host threads (internal host caches -- encoded TMA
+ *     descriptors, kernel attributes -- are mutex-guarded); two calls in flight at once must not
+ *     share a workspace unless they are ordered on one stream.  Calls are CUDA-graph capturable
+ *     (no allocation, no synchronisation, no host reads of device data).
  *   - Errors: a status code is returned and no exception crosses the ABI.  Host-detectable
  *     argument errors return SIGATTN_EINVAL before anything is launched; launch failures return
  *     SIGATTN_ECUDA.  sigattn_last_error() gives a thread-local message for the last failure.
@@ -56,7 +61,11 @@ enum {
                                           for key-split context parallelism (A4)     */
   SIGATTN_F_DQ_F32_PARTIAL = 1u << 2,  /* bwd: dq is float* fp32 alpha*dS K, not finalised
                                           (for the CP reduce-scatter)                        */
-  SIGATTN_F_NO_ZERO_PAD_OUT = 1u << 3, /* caller does not need padded output rows zeroed     */
+  SIGATTN_F_NO_ZERO_PAD_OUT = 1u << 3, /* fwd and bwd: padded output rows (i >= n_q of O, dQ;
+                                          j >= n_k of dK, dV) are left unspecified instead of
+                                          zeroed (saves the fill writes; C3 is 74% padding).
+                                          Valid rows are always written, including the exact
+                                          zeros of a sequence whose key (or query) set is empty. */
   SIGATTN_F_SANITIZE_PAD = 1u << 5,    /* NaN-safe padding: before reading them, the library
                                           zeroes IN PLACE the padded rows of q, k, v (and dout)
                                           that share a 128-row tile with valid rows (rows
@@ -90,10 +99,17 @@ typedef struct {
                         Summed with fp32 atomics: not bitwise reproducible run to run.      */
 } sigattn_params;
 
+/* Bytes of device workspace sigattn_fwd needs (the device work list of visited query tiles:
+ * 16 + 16 * B * H * ceil(Nq / 128) bytes, rounded up to 256).  Returns 0 for invalid params.   */
+size_t sigattn_fwd_workspace_bytes(const sigattn_params* p);
+
 /* Forward (Alg. 1).  q [B,H,Nq,d], k/v [B,H,Nk,d], o [B,H,Nq,d] (fp32 if OUT_F32_PARTIAL).
- * Fully padded query tiles are skipped and the key loop stops at n_k.     */
+ * Fully padded query tiles are skipped and the key loop stops at n_k.
+ * workspace: device, >= sigattn_fwd_workspace_bytes(p), 16-byte aligned, caller-owned; it is
+ * written and read by this call's stream work only (calls on different streams need different
+ * workspaces; calls on one stream may share one).  Returns SIGATTN_EWORKSPACE if too small.    */
 sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k, const void* v,
-                           void* o, void* stream);
+                           void* o, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Bytes of device workspace sigattn_bwd needs (an fp32 dQ accumulator [B,H,Nq,d] plus a
  * small scheduling area).  Returns 0 for invalid params.                                     */

@@ -4,8 +4,8 @@ Hot path: libsigattn.so (include/sigattn.h) -- hand-written tcgen05/TMEM/TMA ker
 This package is the thin Python boundary (argument marshalling) plus the multi-GPU plumbing.
 """
 from .attention import (sigattn_bwd, sigattn_fwd, sigattn_mask_to_seqlens, sigmoid_attention,  # noqa: F401
-                        valid_flops, worklist_host, bwd_workspace_bytes, resolve_bias, sigattn_mask_to_index,
+                        valid_flops, worklist_host, bwd_workspace_bytes, fwd_workspace_bytes, resolve_bias, sigattn_mask_to_index,
                         sigattn_permute_rows)
 
 __all__ = ["sigattn_fwd", "sigattn_bwd", "sigattn_mask_to_seqlens", "sigmoid_attention", "valid_flops",
-           "worklist_host", "bwd_workspace_bytes", "resolve_bias", "sigattn_mask_to_index", "sigattn_permute_rows"]
+           "worklist_host", "bwd_workspace_bytes", "fwd_workspace_bytes", "resolve_bias", "sigattn_mask_to_index", "sigattn_permute_rows"]

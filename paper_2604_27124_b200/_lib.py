@@ -24,7 +24,7 @@ SIGATTN_F_SANITIZE_PAD = 1 << 5
 STATUS_NAMES = {0: "SIGATTN_OK", 1: "SIGATTN_EINVAL", 2: "SIGATTN_EUNSUPPORTED", 3: "SIGATTN_ECUDA",
                 4: "SIGATTN_EWORKSPACE"}
 
-EXPORTED = ["sigattn_fwd", "sigattn_bwd", "sigattn_bwd_workspace_bytes", "sigattn_mask_to_seqlens",
+EXPORTED = ["sigattn_fwd", "sigattn_fwd_workspace_bytes", "sigattn_bwd", "sigattn_bwd_workspace_bytes", "sigattn_mask_to_seqlens",
             "sigattn_valid_flops", "sigattn_worklist_host", "sigattn_last_error", "sigattn_version",
             "sigattn_launch_count", "sigattn_set_profile_events", "sigattn_set_trace_buffer",
             "sigattn_set_debug_counters", "sigattn_mask_to_index", "sigattn_permute_rows"]
@@ -62,8 +62,10 @@ def load():
     lib = ctypes.CDLL(LIB_PATH)
     P = ctypes.POINTER(SigattnParams)
     vp = ctypes.c_void_p
-    lib.sigattn_fwd.argtypes = [P, vp, vp, vp, vp, vp]
+    lib.sigattn_fwd.argtypes = [P, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     lib.sigattn_fwd.restype = ctypes.c_int
+    lib.sigattn_fwd_workspace_bytes.argtypes = [P]
+    lib.sigattn_fwd_workspace_bytes.restype = ctypes.c_size_t
     lib.sigattn_bwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     lib.sigattn_bwd.restype = ctypes.c_int
     lib.sigattn_bwd_workspace_bytes.argtypes = [P]

@@ -104,12 +104,37 @@ def _stream_handle(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def _workspace(ws: Optional[torch.Tensor], need: int, device) -> torch.Tensor:
+    """Caller-owned device workspace of at least `need` bytes (allocated here when not given)."""
+    if ws is None or ws.numel() * ws.element_size() < need:
+        if ws is not None:
+            raise ValueError(f"sigattn: workspace too small ({ws.numel() * ws.element_size()} < {need} bytes)")
+        return torch.empty(max(need, 1), dtype=torch.uint8, device=device)
+    if not ws.is_cuda or ws.device != torch.device(device) or not ws.is_contiguous():
+        raise ValueError("sigattn: workspace must be a contiguous CUDA tensor on the inputs' device")
+    return ws
+
+
+def _check_out(name: str, t: torch.Tensor, shape, dtype, device):
+    if (tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous() or not t.is_cuda
+            or t.device != device):
+        raise ValueError(f"sigattn: {name} must be a contiguous {dtype} CUDA tensor of shape {tuple(shape)} on "
+                         f"{device} (got {tuple(t.shape)} {t.dtype} on {t.device})")
+
+
+def fwd_workspace_bytes(B, H, Nq, Nk, d, dtype=torch.bfloat16) -> int:
+    p = _lib.make_params(B, H, Nq, Nk, d, _lib.SIGATTN_BF16 if dtype == torch.bfloat16 else _lib.SIGATTN_FP16,
+                         None, None, 1.0, 0.0, None, 0)
+    return int(_lib.load().sigattn_fwd_workspace_bytes(ctypes.byref(p)))
+
+
 def sigattn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens_q=None, seqlens_k=None,
                 scale: Optional[float] = None, bias: BiasArg = None, out: Optional[torch.Tensor] = None,
                 out_f32: bool = False, zero_pad_out: bool = True, layout: str = "bhsd",
-                sanitize_pad: bool = False) -> torch.Tensor:
+                sanitize_pad: bool = False, workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Forward (Alg. 1).  Returns O [B, H, Nq, d] ([B, Nq, H, d] for layout='bshd') in q.dtype
-    (fp32 if out_f32: a CP partial)."""
+    (fp32 if out_f32: a CP partial).  workspace: optional uint8 CUDA tensor of at least
+    fwd_workspace_bytes(...) bytes (the device work list), reused across calls on one stream."""
     lib = _lib.load()
     B, H, Nq, Nk, d = _check_qkv(q, k, v, layout)
     sq = _lens(seqlens_q, B, q.device)
@@ -120,13 +145,15 @@ def sigattn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens_q=Non
     oshape = _shape(layout, B, H, Nq, d)
     if out is None:
         out = torch.empty(oshape, dtype=odt, device=q.device)
-    elif out.shape != oshape or out.dtype != odt or not out.is_contiguous():
-        raise ValueError("sigattn: bad out tensor")
+    else:
+        _check_out("out", out, oshape, odt, q.device)
     flags = ((_lib.SIGATTN_F_OUT_F32_PARTIAL if out_f32 else 0) | (0 if zero_pad_out else _lib.SIGATTN_F_NO_ZERO_PAD_OUT)
              | _layout_flag(layout) | (_lib.SIGATTN_F_SANITIZE_PAD if sanitize_pad else 0))
     p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags)
+    need = int(lib.sigattn_fwd_workspace_bytes(ctypes.byref(p)))
+    workspace = _workspace(workspace, need, q.device)
     _lib.check(lib.sigattn_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                               _stream_handle(q.device)))
+                               workspace.data_ptr(), need, _stream_handle(q.device)))
     return out
 
 
@@ -157,20 +184,29 @@ def sigattn_bwd(q, k, v, dout, seqlens_q=None, seqlens_k=None, scale=None, bias:
     sk = _lens(seqlens_k, B, q.device) if seqlens_k is not None else sq if Nk == Nq else None
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     b_scalar, b_tensor = resolve_bias(bias, Nk, sk, B, q.device)
-    dq = torch.empty(_shape(layout, B, H, Nq, d), dtype=torch.float32 if dq_f32 else q.dtype,
-                     device=q.device) if dq is None else dq
-    dk = torch.empty_like(k) if dk is None else dk
-    dv = torch.empty_like(v) if dv is None else dv
+    dq_dtype = torch.float32 if dq_f32 else q.dtype
+    dq_shape = _shape(layout, B, H, Nq, d)
+    if dq is None:
+        dq = torch.empty(dq_shape, dtype=dq_dtype, device=q.device)
+    else:
+        _check_out("dq", dq, dq_shape, dq_dtype, q.device)
+    if dk is None:
+        dk = torch.empty_like(k)
+    else:
+        _check_out("dk", dk, k.shape, k.dtype, q.device)
+    if dv is None:
+        dv = torch.empty_like(v)
+    else:
+        _check_out("dv", dv, v.shape, v.dtype, q.device)
     flags = ((_lib.SIGATTN_F_DQ_F32_PARTIAL if dq_f32 else 0) | (_lib.SIGATTN_F_BWD_DETERMINISTIC if deterministic else 0)
              | _layout_flag(layout) | (_lib.SIGATTN_F_SANITIZE_PAD if sanitize_pad else 0))
     if dbias is not None and (dbias.dtype != torch.float32 or dbias.numel() != B or not dbias.is_contiguous()
-                              or not dbias.is_cuda):
+                              or not dbias.is_cuda or dbias.device != q.device):
         raise ValueError("sigattn: dbias must be a contiguous fp32 CUDA tensor with B entries")
     p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), scale, b_scalar, _ptr(b_tensor), flags,
                          _ptr(dbias))
     need = int(lib.sigattn_bwd_workspace_bytes(ctypes.byref(p)))
-    if workspace is None or workspace.numel() * workspace.element_size() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+    workspace = _workspace(workspace, need, q.device)
     _lib.check(lib.sigattn_bwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
                                dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), workspace.data_ptr(), need,
                                _stream_handle(q.device)))
@@ -279,8 +315,10 @@ class SigmoidAttentionFn(torch.autograd.Function):
         ctx.scale = scale
         ctx.bias = None if isinstance(bias, torch.Tensor) else bias
         ctx.deterministic = deterministic
-        # a [B] bias tensor that requires grad is a learnable per-sequence bias
-        ctx.bias_grad = isinstance(bias, torch.Tensor) and bias.requires_grad and bias.numel() == q.shape[0]
+        # a bias tensor that requires grad is a learnable bias ("fixed or learnable"): one value
+        # per sequence ([B]) or one shared scalar (1 element; its gradient is the sum over sequences)
+        ctx.bias_grad = (isinstance(bias, torch.Tensor) and bias.requires_grad
+                         and bias.numel() in (1, q.shape[0]))
         return o
 
     @staticmethod
@@ -290,7 +328,9 @@ class SigmoidAttentionFn(torch.autograd.Function):
         db = torch.empty(q.shape[0], dtype=torch.float32, device=q.device) if ctx.bias_grad else None
         dq, dk, dv = sigattn_bwd(q, k, v, do.contiguous(), sq, sk, ctx.scale, bias,
                                  deterministic=ctx.deterministic, dbias=db, layout=ctx.layout)
-        dbias = db.to(bt.dtype).reshape(bt.shape) if db is not None else None
+        dbias = None
+        if db is not None:
+            dbias = (db.sum() if bt.numel() == 1 else db).to(bt.dtype).reshape(bt.shape)
         return dq, dk, dv, None, None, None, dbias, None, None
 
 

@@ -101,6 +101,8 @@ struct BwdArgs {
   void* dk;               // [B,H,Nk,D]
   void* dv;
   void* dq_pad;           // 16-bit dQ output whose rows >= ceil128(n_q) the fill warp zeroes, or nullptr
+  int fill_pad;           // 1: zero the padded output rows no tile epilogue writes; 0 (NO_ZERO_PAD_OUT):
+                          //    only the valid rows of sequences with an empty key / query set
   float* dbias;           // [B] fp32, zeroed at entry, += sum of dS (learnable bias gradient); or nullptr
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots (8 events x 512 tiles)
   int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
@@ -783,10 +785,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   }
 
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
-    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0);
-    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0);
+    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0, args.fill_pad);
+    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0, args.fill_pad);
     if (args.dq_pad)   // dq_finalize_kernel covers the rows below
-      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, kBSHD ? 1 : 0);
+      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, kBSHD ? 1 : 0, args.fill_pad);
   }
 
   sm100::tc_fence_before();

@@ -35,6 +35,7 @@ struct DqArgs {
   void* dq;               // bf16/fp16 [B,H,Nq,D], or fp32 when kOutF32 (context-parallel partial)
   int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
   unsigned long long* counters;   // skip accounting (sigattn_set_debug_counters) or nullptr
+  int fill_pad;           // as BwdArgs::fill_pad
 };
 
 template <int D>
@@ -332,7 +333,7 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 
   if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill)   // padded dQ rows beyond the last valid tile
     pad_fill_warp(args.dq, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
-                  kTile, lane, kBSHD ? 1 : 0);
+                  kTile, lane, kBSHD ? 1 : 0, args.fill_pad);
 
   sm100::tc_fence_before();
   __syncthreads();

@@ -341,9 +341,9 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     }
   }
 
-  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill && args.fill_pad)   // padded O rows beyond the last valid tile
+  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill)   // padded O rows beyond the last valid tile
     pad_fill_warp(args.o, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
-                  kTile, lane, args.bshd);
+                  kTile, lane, args.bshd, args.fill_pad);
 
   sm100::tc_fence_before();
   __syncthreads();

@@ -133,24 +133,36 @@ __device__ __forceinline__ size_t row_off(int bshd, int H, int N, int D, int b, 
   return bshd ? ((size_t)((size_t)b * N + row) * H + h) * D : ((size_t)((size_t)b * H + h) * N + row) * D;
 }
 
-// One warp zeroes, for every (b, h) slab it is given, rows [r0, N) of a [B, H, N, row] (or, with
-// bshd, [B, N, H, row]) tensor of row_bytes-long rows:
-// r0 = 0 when the sequence has no work item (n_own == 0 or n_other == 0), else min(ceil_gran(n_own), N)
-// -- the rows below r0 are written (padded rows as zeros) by the tile epilogues.  Slabs are strided
-// over the grid; the idle warp of each persistent attention CTA runs this alongside the main work.
+// One warp zeroes, for every (b, h) slab it is given, rows [r0, r1) of a [B, H, N, row] (or, with
+// bshd, [B, N, H, row]) tensor of row_bytes-long rows.
+//   pad_rows = 1: r1 = N; r0 = 0 when the sequence has no work item (n_own == 0 or n_other == 0),
+//                 else min(ceil_gran(n_own), N) -- the rows below r0 are written (padded rows as
+//                 zeros) by the tile epilogues.
+//   pad_rows = 0 (SIGATTN_F_NO_ZERO_PAD_OUT: padded rows are left as they are): only the VALID rows
+//                 no epilogue writes, [0, n_own) of a sequence with n_other == 0 -- an empty key (or
+//                 query) set gives exact-zero valid outputs (empty sums, Eq. 2).
+// Slabs are strided over the grid; the idle warp of each persistent attention CTA runs this
+// alongside the main work.
 __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, int H, int N,
                                               const int32_t* __restrict__ lens_own,
                                               const int32_t* __restrict__ lens_other, int N_other, int gran,
-                                              uint32_t lane, int bshd = 0) {
+                                              uint32_t lane, int bshd = 0, int pad_rows = 1) {
   const uint4 z = make_uint4(0, 0, 0, 0);
   const int cpr = row_bytes / 16;   // 16-byte chunks per row
   for (int zh = blockIdx.x; zh < B * H; zh += gridDim.x) {
     const int b = zh / H, h = zh - b * H;
     const int n = clamp_len(lens_own, b, N), m = clamp_len(lens_other, b, N_other);
-    const int r0 = (n == 0 || m == 0) ? 0 : min((n + gran - 1) / gran * gran, N);
-    if (r0 >= N) continue;
+    int r0, r1;
+    if (pad_rows) {
+      r0 = (n == 0 || m == 0) ? 0 : min((n + gran - 1) / gran * gran, N);
+      r1 = N;
+    } else {
+      r0 = 0;
+      r1 = m == 0 ? n : 0;
+    }
+    if (r0 >= r1) continue;
     if (!bshd) {
-      const long long total = (long long)(N - r0) * cpr;
+      const long long total = (long long)(r1 - r0) * cpr;
       uint4* base = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out) + ((size_t)zh * N + r0) * row_bytes);
       for (long long i = lane; i < total; i += 32) base[i] = z;
     } else {
@@ -159,7 +171,7 @@ __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, i
       uint8_t* base = reinterpret_cast<uint8_t*>(out) + ((size_t)b * N * H + h) * row_bytes;
       const size_t rs = (size_t)H * row_bytes;
       const int step = 32 / cpr, lr = (int)lane / cpr, c = (int)lane % cpr;
-      for (int r = r0 + lr; r < N; r += step) reinterpret_cast<uint4*>(base + (size_t)r * rs)[c] = z;
+      for (int r = r0 + lr; r < r1; r += step) reinterpret_cast<uint4*>(base + (size_t)r * rs)[c] = z;
     }
   }
 }
@@ -214,12 +226,13 @@ __device__ __forceinline__ void dq_finalize_rows(const float* __restrict__ acc, 
 template <bool kBf16>
 __global__ void dq_finalize_kernel(const float* __restrict__ acc, uint16_t* __restrict__ dq, int H, int N, int D,
                                    const int32_t* __restrict__ lens, const int32_t* __restrict__ lens_k, int Nk,
-                                   int bshd) {
+                                   int bshd, int pad_rows) {
   const int zh = blockIdx.y;
   const int nq = clamp_len(lens, zh / H, N), nk = clamp_len(lens_k, zh / H, Nk);
   // rows from ceil128(n_q) on (all rows if the sequence has no work) are zeroed by the backward
   // kernel's fill warp; finalise the rest
-  const int rlim = (nq == 0 || nk == 0) ? 0 : min((nq + 127) & ~127, N);
+  // (pad_rows = 0, SIGATTN_F_NO_ZERO_PAD_OUT: the valid rows only)
+  const int rlim = (nq == 0 || nk == 0) ? 0 : (pad_rows ? min((nq + 127) & ~127, N) : nq);
   const int rows = (rlim + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * rows, r1 = min(rlim, r0 + rows);
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;

@@ -79,8 +79,8 @@ EncodeTiledFn get_encode() {
 // layout: 4-D view {d, rows, H, B}.  Box {64 elements = 128 B, box_rows, 1(, 1)}, 128-byte
 // swizzle: exactly the UMMA K-major / MN-major SWIZZLE_128B atom whichever the layout.  Rows past
 // `rows` read as zero (OOB fill), so a ragged last tile never touches another head's or sequence's data.
-sigattn_status make_tmap(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int elem_bytes, int d, int rows,
-                         int B, int H, bool bshd, int box_rows = 128) {
+sigattn_status encode_tmap(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int elem_bytes, int d, int rows,
+                           int B, int H, bool bshd, int box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(SIGATTN_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const cuuint64_t e = (cuuint64_t)elem_bytes, dd = (cuuint64_t)d, n = (cuuint64_t)rows, hh = (cuuint64_t)H;
@@ -94,6 +94,45 @@ sigattn_status make_tmap(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SIGATTN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return SIGATTN_OK;
+}
+
+// Small cache of encoded tensor maps keyed by (pointer, geometry): a training loop calls the
+// library with the same buffers step after step, and encoding 3-5 maps per call costs host time
+// on the launch path.  The map is a pure function of its key (it holds no other state), so a hit
+// is exactly the map encode_tmap would produce.  Bounded: kTmapCacheSize entries, replaced round
+// robin; guarded by a mutex (calls are reentrant).
+struct TmapKey {
+  const void* ptr;
+  int dt, elem_bytes, d, rows, B, H, bshd, box_rows;
+  bool operator==(const TmapKey& o) const {
+    return ptr == o.ptr && dt == o.dt && elem_bytes == o.elem_bytes && d == o.d && rows == o.rows && B == o.B &&
+           H == o.H && bshd == o.bshd && box_rows == o.box_rows;
+  }
+};
+constexpr int kTmapCacheSize = 64;
+
+sigattn_status make_tmap(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int elem_bytes, int d, int rows,
+                         int B, int H, bool bshd, int box_rows = 128) {
+  static std::mutex mu;
+  static TmapKey keys[kTmapCacheSize];
+  static CUtensorMap maps[kTmapCacheSize];
+  static int used = 0, next = 0;
+  const TmapKey key{ptr, (int)dt, elem_bytes, d, rows, B, H, bshd ? 1 : 0, box_rows};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < used; ++i)
+      if (keys[i] == key) {
+        *m = maps[i];
+        return SIGATTN_OK;
+      }
+  }
+  sigattn_status st = encode_tmap(m, ptr, dt, elem_bytes, d, rows, B, H, bshd, box_rows);
+  if (st != SIGATTN_OK) return st;
+  std::lock_guard<std::mutex> lock(mu);
+  const int slot = used < kTmapCacheSize ? used++ : (next++ % kTmapCacheSize);
+  keys[slot] = key;
+  maps[slot] = *m;
   return SIGATTN_OK;
 }
 
@@ -123,9 +162,22 @@ sigattn_status check_params(const sigattn_params* p) {
   return SIGATTN_OK;
 }
 
+// cudaFuncSetAttribute once per (kernel, device, size): it is a host call on every launch path otherwise.
 template <typename K>
 sigattn_status set_smem(K kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, std::pair<int, int>>> done;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  const void* key = reinterpret_cast<const void*>(kernel);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : done)
+      if (e.first == key && e.second.first == dev && e.second.second >= bytes) return SIGATTN_OK;
+  }
   CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  std::lock_guard<std::mutex> lock(mu);
+  done.push_back({key, {dev, bytes}});
   return SIGATTN_OK;
 }
 
@@ -237,6 +289,7 @@ sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* 
   a.dk = dk;
   a.dv = dv;
   a.dq_pad = dq_pad;
+  a.fill_pad = (p->flags & SIGATTN_F_NO_ZERO_PAD_OUT) ? 0 : 1;
   a.dbias = p->dbias;
   a.trace = g_trace;
   a.counters = g_counters;
@@ -286,6 +339,7 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   a.dk = dk;
   a.dv = dv;
   a.dq_pad = dq_pad;
+  a.fill_pad = (p->flags & SIGATTN_F_NO_ZERO_PAD_OUT) ? 0 : 1;
   a.dbias = p->dbias;
   a.trace = g_trace;
   a.counters = g_counters;
@@ -342,6 +396,7 @@ sigattn_status launch_dq(const sigattn_params* p, const void* q, const void* k, 
   a.dq = dq;
   a.bshd = layout_bshd(p) ? 1 : 0;
   a.counters = g_counters;
+  a.fill_pad = (p->flags & SIGATTN_F_NO_ZERO_PAD_OUT) ? 0 : 1;
   using C = DqCfg<D>;
   auto kern = layout_bshd(p) ? sigattn_dq_kernel<D, kBf16, kF32, true> : sigattn_dq_kernel<D, kBf16, kF32, false>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
@@ -363,34 +418,14 @@ sigattn_status sanitize_pad(const sigattn_params* p, const void* t, int N, const
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// Small device scratch for the forward work list, cached per (device, stream) so that calls on
-// one stream reuse it in stream order and calls on different streams never share it.  Grows
-// geometrically; a replaced buffer is released with cudaFreeAsync on its own stream (after the
-// work that used it).  This is the only memory the library owns.
-sigattn_status get_scratch(cudaStream_t s, size_t bytes, void** out) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> cache;
-  int dev = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lock(mu);
-  auto& e = cache[{dev, s}];
-  if (e.second < bytes) {
-    if (e.first) cudaFreeAsync(e.first, s);
-    size_t nb = std::max(bytes, 2 * e.second);
-    nb = align_up(std::max<size_t>(nb, 1 << 16), 1 << 16);
-    void* p = nullptr;
-    CUDA_TRY(cudaMallocAsync(&p, nb, s));
-    e = {p, nb};
-  }
-  *out = e.first;
-  return SIGATTN_OK;
-}
-
 size_t ws_acc_bytes(const sigattn_params* p) { return align_up((size_t)p->B * p->H * p->Nq * p->d * sizeof(float), 256); }
 size_t ws_items_bytes(const sigattn_params* p) {
   return align_up(16 + (size_t)p->B * p->H * cdiv(p->Nk, 128) * sizeof(int4), 256);
 }
 size_t ws_items_q_bytes(const sigattn_params* p) {   // query-tile work list (deterministic dQ pass)
+  return align_up(16 + (size_t)p->B * p->H * cdiv(p->Nq, 128) * sizeof(int4), 256);
+}
+size_t ws_fwd_bytes(const sigattn_params* p) {   // forward work list: {count, pad} + items
   return align_up(16 + (size_t)p->B * p->H * cdiv(p->Nq, 128) * sizeof(int4), 256);
 }
 
@@ -456,15 +491,22 @@ int64_t sigattn_worklist_host(int kind, int B, int H, int Nq, int Nk, const int3
   return n;
 }
 
+size_t sigattn_fwd_workspace_bytes(const sigattn_params* p) {
+  if (check_params(p) != SIGATTN_OK) return 0;
+  return ws_fwd_bytes(p);
+}
+
 sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k, const void* v, void* o,
-                           void* stream) {
+                           void* workspace, size_t workspace_bytes, void* stream) {
   sigattn_status st = check_params(p);
   if (st != SIGATTN_OK) return st;
-  if (!q || !k || !v || !o) return fail(SIGATTN_EINVAL, "null tensor pointer");
-  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
-    return fail(SIGATTN_EINVAL, "tensor pointers must be 16-byte aligned");
+  if (!q || !k || !v || !o || !workspace) return fail(SIGATTN_EINVAL, "null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(workspace))
+    return fail(SIGATTN_EINVAL, "pointers must be 16-byte aligned");
+  if (workspace_bytes < ws_fwd_bytes(p))
+    return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(ws_fwd_bytes(p)) + " bytes");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  {
+  {   // every host-detectable error is reported above, before anything is launched
     const int32_t* lk = p->seqlens_k;   // NULL: all keys valid
     if ((st = sanitize_pad(p, q, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
     if ((st = sanitize_pad(p, k, p->Nk, lk, s)) != SIGATTN_OK) return st;
@@ -472,11 +514,8 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
   }
   const bool f32 = (p->flags & SIGATTN_F_OUT_F32_PARTIAL) != 0;
   const int max_items = p->B * p->H * cdiv(p->Nq, 128);
-  void* scratch = nullptr;
-  const size_t bytes = 16 + (size_t)max_items * sizeof(int4);
-  if ((st = get_scratch(s, bytes, &scratch)) != SIGATTN_OK) return st;
-  int* n_items = reinterpret_cast<int*>(scratch);
-  int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(scratch) + 16);
+  int* n_items = reinterpret_cast<int*>(workspace);
+  int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(workspace) + 16);
   st = launch_worklist(use_fwd2(p->d) ? 2 : 0, p, items, n_items, s);
   if (st == SIGATTN_OK) {
     const bool bf = p->dtype == SIGATTN_BF16;
@@ -514,17 +553,17 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   const size_t need = sigattn_bwd_workspace_bytes(p);
   if (workspace_bytes < need)
     return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  const bool dq_f32 = (p->flags & SIGATTN_F_DQ_F32_PARTIAL) != 0;
+  if (dq_f32 && layout_bshd(p))
+    return fail(SIGATTN_EUNSUPPORTED, "SIGATTN_F_DQ_F32_PARTIAL needs the [B, H, N, d] layout");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  {
+  {   // every host-detectable error is reported above, before anything is launched
     const int32_t* lk = p->seqlens_k;   // NULL: all keys valid
     if ((st = sanitize_pad(p, q, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
     if ((st = sanitize_pad(p, dout, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
     if ((st = sanitize_pad(p, k, p->Nk, lk, s)) != SIGATTN_OK) return st;
     if ((st = sanitize_pad(p, v, p->Nk, lk, s)) != SIGATTN_OK) return st;
   }
-  const bool dq_f32 = (p->flags & SIGATTN_F_DQ_F32_PARTIAL) != 0;
-  if (dq_f32 && layout_bshd(p))
-    return fail(SIGATTN_EUNSUPPORTED, "SIGATTN_F_DQ_F32_PARTIAL needs the [B, H, N, d] layout");
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   const bool bf = p->dtype == SIGATTN_BF16;
   if (p->flags & SIGATTN_F_BWD_DETERMINISTIC) {
@@ -577,10 +616,12 @@ sigattn_status sigattn_bwd(const sigattn_params* p, const void* q, const void* k
   const dim3 grid(std::max(1, std::min(32, cdiv(p->Nq, 512))), p->B * p->H);
   if (bf)
     dq_finalize_kernel<true><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
-                                                  p->seqlens_q, p->seqlens_k, p->Nk, layout_bshd(p) ? 1 : 0);
+                                                  p->seqlens_q, p->seqlens_k, p->Nk, layout_bshd(p) ? 1 : 0,
+                                                  (p->flags & SIGATTN_F_NO_ZERO_PAD_OUT) ? 0 : 1);
   else
     dq_finalize_kernel<false><<<grid, 256, 0, s>>>(dq_acc, reinterpret_cast<uint16_t*>(dq), p->H, p->Nq, p->d,
-                                                   p->seqlens_q, p->seqlens_k, p->Nk, layout_bshd(p) ? 1 : 0);
+                                                   p->seqlens_q, p->seqlens_k, p->Nk, layout_bshd(p) ? 1 : 0,
+                                                  (p->flags & SIGATTN_F_NO_ZERO_PAD_OUT) ? 0 : 1);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;

@@ -119,15 +119,19 @@ def test_fwd_rejects_bad_params_before_launch(kw, status):
     lib = _lib.load()
     p = _params(**kw)
     fake = 1 << 20
-    assert lib.sigattn_fwd(ctypes.byref(p), fake, fake, fake, fake, None) == status
+    assert lib.sigattn_fwd(ctypes.byref(p), fake, fake, fake, fake, fake, 1 << 20, None) == status
     assert len(lib.sigattn_last_error()) > 0
 
 
 def test_pointer_checks():
     lib = _lib.load()
     p = _params()
-    assert lib.sigattn_fwd(ctypes.byref(p), None, 16, 16, 16, None) == 1            # null
-    assert lib.sigattn_fwd(ctypes.byref(p), 24, 16, 16, 16, None) == 1              # misaligned
+    fneed = lib.sigattn_fwd_workspace_bytes(ctypes.byref(p))
+    assert fneed >= 16 + 16 and fneed % 256 == 0
+    assert lib.sigattn_fwd(ctypes.byref(p), None, 16, 16, 16, 16, fneed, None) == 1   # null
+    assert lib.sigattn_fwd(ctypes.byref(p), 24, 16, 16, 16, 16, fneed, None) == 1     # misaligned
+    assert lib.sigattn_fwd(ctypes.byref(p), 16, 16, 16, 16, None, fneed, None) == 1   # no workspace
+    assert lib.sigattn_fwd(ctypes.byref(p), 16, 16, 16, 16, 16, fneed - 1, None) == 4  # workspace too small
     need = lib.sigattn_bwd_workspace_bytes(ctypes.byref(p))
     assert need >= 128 * 64 * 4
     assert lib.sigattn_bwd(ctypes.byref(p), 16, 16, 16, 16, 16, 16, 16, 16, need - 1, None) == 4
@@ -149,3 +153,22 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(ImportError, match="no CPU fallback"):
         _lib.load()
+
+
+def test_c_program_links_against_header(tmp_path):
+    """A plain C99 program built against include/sigattn.h and linked to libsigattn.so runs the
+    host-side entry points (tests/c/abi_test.c) -- the ABI is usable without Python or torch."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    lib = _lib.load() and _lib.LIB_PATH
+    exe = tmp_path / "abi_test"
+    libdir = os.path.dirname(lib)
+    subprocess.check_call([cc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "c", "abi_test.c"), "-L", libdir, "-l:" + os.path.basename(lib),
+                           "-Wl,-rpath," + libdir, "-o", str(exe)])
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "abi_test: OK" in r.stdout

@@ -515,17 +515,46 @@ def test_layout_bshd_autograd():
 
 def test_encoder_layer_integration():
     """§8f f4: the op inside Table 4's pre-LN encoder layer (hidden 768, 12 heads, d = 64), bf16,
-    jagged lengths, [B, N, H, d] projections read in place; forward and input/weight gradients
-    against the same layer composed in plain PyTorch fp32 (sigmoid attention written out)."""
-    from paper_2604_27124_b200.encoder import SigmoidEncoderLayer, reference_attention_fp32
+    jagged lengths, [B, N, H, d] projections read in place.
+    (1) The layer's own attention call -- the q/k/v projection outputs it produced, the output it
+        fed to o_proj, the incoming gradient dO and the dQ/dK/dV it returned, captured with hooks --
+        against the fp64 oracle (fwd and bwd), every element.
+    (2) Forward and input/weight gradients of the whole layer against the same layer composed in
+        plain PyTorch fp32 (tests/encoder_ref.py, test-only), for the surrounding plumbing."""
+    from paper_2604_27124_b200.encoder import SigmoidEncoderLayer
+    from encoder_ref import reference_attention_fp32
     torch.manual_seed(5)
     layer = SigmoidEncoderLayer(dropout=0.0).cuda().to(torch.bfloat16)
     B, N = 3, 384
     lens = torch.tensor([384, 200, 57], dtype=torch.int32, device="cuda")
     x = torch.randn(B, N, 768, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    cap = {}
+
+    def keep(name):
+        def fwd_hook(mod, inp, out):
+            cap[name] = out.detach()
+            out.register_hook(lambda g: cap.__setitem__("d" + name, g.detach()))
+        return fwd_hook
+
+    def keep_o(mod, inp):
+        cap["o"] = inp[0].detach()
+        inp[0].register_hook(lambda g: cap.__setitem__("do", g.detach()))
+
+    hooks = [layer.q_proj.register_forward_hook(keep("q")), layer.k_proj.register_forward_hook(keep("k")),
+             layer.v_proj.register_forward_hook(keep("v")), layer.o_proj.register_forward_pre_hook(keep_o)]
     y = layer(x, lens)
     gy = torch.randn_like(y)
     y.backward(gy)
+    for h_ in hooks:
+        h_.remove()
+    bhsd = lambda t: f64(t.reshape(B, N, 12, 64).transpose(1, 2))  # noqa: E731
+    nl = lens.tolist()
+    bias = np.full(B, -math.log(N))
+    ro = oracle.fwd(bhsd(cap["q"]), bhsd(cap["k"]), bhsd(cap["v"]), nl, nl, 1 / 8, bias)
+    assert relerr(bhsd(cap["o"]), ro) <= BF16_TOL
+    rdq, rdk, rdv = oracle.bwd(bhsd(cap["q"]), bhsd(cap["k"]), bhsd(cap["v"]), bhsd(cap["do"]), nl, nl, 1 / 8, bias)
+    for name, ref in (("dq", rdq), ("dk", rdk), ("dv", rdv)):
+        assert relerr(bhsd(cap[name]), ref) <= BF16_TOL, name
     layer_f = SigmoidEncoderLayer(dropout=0.0).cuda()   # fp32 copy of the same (bf16) weights
     layer_f.load_state_dict({k_: v_.float() for k_, v_ in layer.state_dict().items()})
     xr = x.detach().float().requires_grad_(True)
@@ -631,3 +660,74 @@ def test_nonprefix_key_padding_mask(d):
     for bb in range(B):   # stable: valid positions in order, then padded positions in order
         ref_idx = torch.cat([(~mask[bb]).nonzero().flatten(), mask[bb].nonzero().flatten()]).to(torch.int32)
         assert torch.equal(idx[bb], ref_idx)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("deterministic", [False, True])
+def test_no_zero_pad_out_valid_rows(d, deterministic):
+    """SIGATTN_F_NO_ZERO_PAD_OUT leaves padded rows unspecified, but every VALID row is written --
+    including the exact zeros of a sequence whose key set is empty (n_k = 0 < n_q) or whose query set
+    is empty (dK = dV = 0 on its valid keys).  Outputs are prefilled with NaN."""
+    sa = _sa()
+    cfg = I.Config("nozero", B=4, H=2, N=320, d=d, lengths=[320, 77, 5, 0], Nk=256, lengths_k=[256, 0, 129, 200],
+                   seed=60 + d)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    alpha, b = 1.0 / math.sqrt(d), -math.log(256)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b, out=torch.full_like(q, float("nan")), zero_pad_out=False)
+    p = sa.attention
+    dq, dk, dv = (torch.full_like(t, float("nan")) for t in (q, k, v))
+    flags = p._lib.SIGATTN_F_NO_ZERO_PAD_OUT | (p._lib.SIGATTN_F_BWD_DETERMINISTIC if deterministic else 0)
+    lib = p._lib.load()
+    prm = p._lib.make_params(cfg.B, cfg.H, cfg.N, cfg.N_k, d, 0, nq.data_ptr(), nk.data_ptr(), alpha, b, None, flags)
+    need = int(lib.sigattn_bwd_workspace_bytes(__import__("ctypes").byref(prm)))
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    p._lib.check(lib.sigattn_bwd(__import__("ctypes").byref(prm), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                 do.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), need,
+                                 torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    bias = np.full(cfg.B, b)
+    ro = oracle.fwd(f64(q), f64(k), f64(v), cfg.nq, cfg.nk, alpha, bias)
+    rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, alpha, bias)
+    for name, got, ref, lens in (("o", o, ro, cfg.nq), ("dq", dq, rdq, cfg.nq), ("dk", dk, rdk, cfg.nk),
+                                 ("dv", dv, rdv, cfg.nk)):
+        g = f64(got)
+        for bb in range(cfg.B):
+            valid = g[bb, :, :lens[bb]]
+            assert np.isfinite(valid).all(), f"{name}: valid rows of sequence {bb} not written"
+            assert np.abs(valid - ref[bb, :, :lens[bb]]).max(initial=0) <= BF16_TOL * np.abs(ref).max()
+    assert torch.all(o[1, :, :77] == 0), "n_k = 0: valid O rows are exact zeros"
+    assert torch.all(dk[3, :, :200] == 0) and torch.all(dv[3, :, :200] == 0), "n_q = 0: dK = dV = 0"
+
+
+def test_scalar_learnable_bias_gradient_b_gt_1():
+    """A 1-element learnable bias shared by all sequences (B > 1) gets d loss / d b = sum over
+    sequences of the per-sequence gradient (it used to get None)."""
+    sa = _sa()
+    cfg = I.Config("db_scalar", B=3, H=2, N=256, d=64, lengths=[256, 100, 17], seed=43)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    bias = torch.tensor([-4.5], device="cuda", requires_grad=True)
+    o = sa.sigmoid_attention(q, k, v, seqlens_q=nq, seqlens_k=nk, bias=bias)
+    o.backward(do)
+    assert bias.grad is not None and bias.grad.shape == (1,)
+    ref = oracle.dbias(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, 1 / 8, [-4.5] * 3).sum()
+    assert abs(float(bias.grad.item()) - ref) <= 1e-2 * abs(ref)
+
+
+def test_output_buffer_validation():
+    """Caller-supplied outputs / workspaces of the wrong shape, dtype or size are rejected before any
+    launch (a bf16 dq with dq_f32 used to be memset as fp32)."""
+    sa = _sa()
+    cfg = I.Config("val", B=2, H=2, N=256, d=64, seed=44)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    with pytest.raises(ValueError, match="dq"):
+        sa.sigattn_bwd(q, k, v, do, dq=torch.empty_like(q), dq_f32=True)
+    with pytest.raises(ValueError, match="dk"):
+        sa.sigattn_bwd(q, k, v, do, dk=torch.empty(2, 2, 128, 64, dtype=q.dtype, device="cuda"))
+    with pytest.raises(ValueError, match="dv"):
+        sa.sigattn_bwd(q, k, v, do, dv=torch.empty_like(v).transpose(2, 3).contiguous().transpose(2, 3))
+    with pytest.raises(ValueError, match="out"):
+        sa.sigattn_fwd(q, k, v, out=torch.empty_like(q, dtype=torch.float32))
+    with pytest.raises(ValueError, match="workspace too small"):
+        sa.sigattn_fwd(q, k, v, workspace=torch.empty(16, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(ValueError, match="workspace too small"):
+        sa.sigattn_bwd(q, k, v, do, workspace=torch.empty(16, dtype=torch.uint8, device="cuda"))
