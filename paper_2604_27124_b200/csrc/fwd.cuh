@@ -27,6 +27,9 @@
 #ifndef SIGATTN_DBG_FWD_NOSIGMA
 #define SIGATTN_DBG_FWD_NOSIGMA 0
 #endif
+#ifndef SIGATTN_DBG_FWD_NOTMA_KV
+#define SIGATTN_DBG_FWD_NOTMA_KV 0   // timing experiments only (wrong results): K/V tiles loaded once per slot, then reused
+#endif
 #ifndef SIGATTN_FWD_SPEC
 #define SIGATTN_FWD_SPEC 1  // tier-4 sigma evaluated before the warp vote (sigma_row_spec4)
 #endif
@@ -222,19 +225,27 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (sm100::elect_one()) {
           sm100::trace_event(args.trace, kv_it, 512);
           uint8_t* ks = smem + C::kKOff + st * C::kTileBytes;
-          sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
+          if (SIGATTN_DBG_FWD_NOTMA_KV && kv_it >= (uint32_t)C::kStages) {
+            sm100::mbar_arrive(&k_full[st]);
+          } else {
+            sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
-          for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_bh(ks + s * (kTile * 128), &tmK, &k_full[st], s * 64, j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+            for (int s = 0; s < C::kSub; ++s)
+              sm100::tma_load_bh(ks + s * (kTile * 128), &tmK, &k_full[st], s * 64, j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+          }
         }
         __syncwarp();
         sm100::mbar_wait_backoff(&v_empty[st], ph ^ 1);
         if (sm100::elect_one()) {
           uint8_t* vs = smem + C::kVOff + st * C::kTileBytes;
-          sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
+          if (SIGATTN_DBG_FWD_NOTMA_KV && kv_it >= (uint32_t)C::kStages) {
+            sm100::mbar_arrive(&v_full[st]);
+          } else {
+            sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
-          for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_bh(vs + s * (kTile * 128), &tmV, &v_full[st], s * 64, j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+            for (int s = 0; s < C::kSub; ++s)
+              sm100::tma_load_bh(vs + s * (kTile * 128), &tmV, &v_full[st], s * 64, j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+          }
         }
         __syncwarp();
       }

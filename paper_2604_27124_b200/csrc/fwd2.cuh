@@ -134,20 +134,28 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         const uint32_t st = kv_it % C::kStages, ph = (kv_it / C::kStages) & 1;
         sm100::mbar_wait_backoff(&k_empty[st], ph ^ 1);
         if (sm100::elect_one()) {
-          sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
+          if (SIGATTN_DBG_FWD_NOTMA_KV && kv_it >= (uint32_t)C::kStages) {
+            sm100::mbar_arrive(&k_full[st]);
+          } else {
+            sm100::mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
-          for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_bh(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
-                               j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+            for (int s = 0; s < C::kSub; ++s)
+              sm100::tma_load_bh(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
+                                 j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+          }
         }
         __syncwarp();
         sm100::mbar_wait_backoff(&v_empty[st], ph ^ 1);
         if (sm100::elect_one()) {
-          sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
+          if (SIGATTN_DBG_FWD_NOTMA_KV && kv_it >= (uint32_t)C::kStages) {
+            sm100::mbar_arrive(&v_full[st]);
+          } else {
+            sm100::mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
-          for (int s = 0; s < C::kSub; ++s)
-            sm100::tma_load_bh(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
-                               j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+            for (int s = 0; s < C::kSub; ++s)
+              sm100::tma_load_bh(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
+                                 j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+          }
         }
         __syncwarp();
       }
@@ -277,7 +285,10 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&s_free[x]);
           }
-          if (C::kSepP) {   // S already released: no reload possible, vote-first tiers
+          if (SIGATTN_DBG_FWD_NOSIGMA) {   // timing experiments only: P = bits of S, no sigma work
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[e] = __float_as_uint(r[2 * e]) ^ __float_as_uint(r[2 * e + 1]);
+          } else if (C::kSepP) {   // S already released: no reload possible, vote-first tiers
             if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
             else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
           } else {

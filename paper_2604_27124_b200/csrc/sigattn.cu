@@ -26,6 +26,8 @@
 #define SIGATTN_FWD2_MIN_D 128
 #endif
 constexpr bool use_fwd2(int d) { return d >= SIGATTN_FWD2_MIN_D; }
+// work-list kind of the forward: pairs of query tiles (2) or single query tiles (0)
+constexpr int fwd_item_kind(int d) { return use_fwd2(d) ? 2 : 0; }
 #include "fwd.cuh"
 #include "sched.cuh"
 
@@ -516,7 +518,7 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
   const int max_items = p->B * p->H * cdiv(p->Nq, 128);
   int* n_items = reinterpret_cast<int*>(workspace);
   int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(workspace) + 16);
-  st = launch_worklist(use_fwd2(p->d) ? 2 : 0, p, items, n_items, s);
+  st = launch_worklist(fwd_item_kind(p->d), p, items, n_items, s);
   if (st == SIGATTN_OK) {
     const bool bf = p->dtype == SIGATTN_BF16;
     if (p->d == 64) {

@@ -224,4 +224,5 @@ __device__ __forceinline__ int sigma_row(float (&v)[N], float a, float c, bool l
   }
 }
 
+
 }  // namespace sigattn

@@ -461,4 +461,17 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   else return pack_f16(lo, hi);
 }
 
+
+// ------------------------------------------------------------------ register reallocation
+// Per-warpgroup register budget (all four warps of a warpgroup execute it): the issuer / producer
+// warpgroup gives registers back, the compute warpgroups take them (64K registers per SM).
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+
 }  // namespace sm100
