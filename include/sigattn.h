@@ -175,6 +175,58 @@ void sigattn_set_trace_buffer(void* device_buffer);
  * The caller zeroes them; one atomic per work item.  NULL disables.                               */
 void sigattn_set_debug_counters(void* device_counters);
 
+/* ---------------------------------------------------------------------------------------------
+ * Key-split context parallelism with the reduction fused into the kernels.
+ * Sigmoid weights are additive over key blocks (sec. 3): with the SAME bias b,
+ *   O = sum_r sigma(alpha Q K_r^T + b) V_r,   dQ = sum_r alpha dS_r K_r,
+ * so G ranks that each hold one key block need no log-sum-exp merge -- only a sum.  Rank g owns
+ * query rows [g Nq/G, (g+1) Nq/G) and an fp32 accumulator [B, H, Nq/G, d] for them.  The fused
+ * calls below reduce-add (red.global.add.v4.f32, system scope) every partial row straight into the
+ * owner's accumulator from the kernel epilogue -- over NVLink when the owner is another GPU --
+ * instead of materialising a partial [B, H, Nq, d] tensor and reduce-scattering it afterwards.
+ *
+ * Per-rank problem in sigattn_params: Nq = the full query length (all queries, e.g. all-gathered
+ * Q), Nk = this rank's key block length, seqlens_q = global valid lengths, seqlens_k = the valid
+ * keys of this rank's block, bias = the GLOBAL b (e.g. -log of the global length, never the block
+ * length; DESIGN reading R1).  Layout [B, H, N, d] only.
+ * Protocol (the caller's, e.g. paper_2604_27124_b200.parallel): every rank zeroes its accumulator,
+ * all ranks synchronise, each rank runs the fused call, all ranks synchronise again (the kernels end
+ * with a system-scope fence), then each rank runs sigattn_cp_finalize on its own accumulator.    */
+typedef struct {
+  int world;               /* G >= 1; Nq must be a multiple of G                                   */
+  int rank;                /* this rank, 0 <= rank < G                                             */
+  float* const* peer_acc;  /* DEVICE array [G] of device pointers: rank g's fp32 accumulator
+                              [B, H, Nq/G, d] (this rank's own at [rank]), mapped on this device
+                              (sigattn_ipc_import for other processes' buffers)                    */
+} sigattn_cp_params;
+
+/* Forward partial over this rank's keys, reduce-added into the owners' accumulators (unscaled fp32
+ * sums of P V, padded query rows contribute nothing).  workspace >= sigattn_fwd_workspace_bytes(p). */
+sigattn_status sigattn_fwd_cp(const sigattn_params* p, const sigattn_cp_params* cp, const void* q,
+                              const void* k, const void* v, void* workspace, size_t workspace_bytes,
+                              void* stream);
+/* Bytes of workspace sigattn_bwd_cp needs (the scheduling area only: dQ goes to the peers).      */
+size_t sigattn_bwd_cp_workspace_bytes(const sigattn_params* p);
+/* Backward over this rank's keys: dk, dv [B, H, Nk, d] of this rank's block are complete on return
+ * (keys are owned; padded rows 0 as in sigattn_bwd); alpha dS K of every valid query row is
+ * reduce-added into the owners' fp32 dQ accumulators.  dout is the full [B, H, Nq, d].            */
+sigattn_status sigattn_bwd_cp(const sigattn_params* p, const sigattn_cp_params* cp, const void* q,
+                              const void* k, const void* v, const void* dout, void* dk, void* dv,
+                              void* workspace, size_t workspace_bytes, void* stream);
+/* acc [B, H, Nq/G, d] fp32 (this rank's accumulator, complete) -> out [B, H, Nq/G, d] in p->dtype;
+ * rows whose global index rank * Nq/G + r is >= n_q[b] are written as exact 0.                   */
+sigattn_status sigattn_cp_finalize(const sigattn_params* p, int world, int rank, const float* acc, void* out,
+                                   void* stream);
+
+/* CUDA IPC of a device buffer between processes (for sigattn_cp_params.peer_acc): export writes
+ * sigattn_ipc_handle_bytes() bytes (the allocation's cudaIpcMemHandle_t and the pointer's offset in
+ * it); import maps it on the current device (peer access over NVLink when it lives on another
+ * GPU) and returns the pointer; close unmaps a pointer returned by import.                       */
+size_t sigattn_ipc_handle_bytes(void);
+sigattn_status sigattn_ipc_export(const void* dev_ptr, void* handle);
+sigattn_status sigattn_ipc_import(const void* handle, void** dev_ptr);
+sigattn_status sigattn_ipc_close(void* dev_ptr);
+
 const char* sigattn_last_error(void); /* thread-local message of the last failing call */
 const char* sigattn_version(void);
 

@@ -27,7 +27,9 @@ STATUS_NAMES = {0: "SIGATTN_OK", 1: "SIGATTN_EINVAL", 2: "SIGATTN_EUNSUPPORTED",
 EXPORTED = ["sigattn_fwd", "sigattn_fwd_workspace_bytes", "sigattn_bwd", "sigattn_bwd_workspace_bytes", "sigattn_mask_to_seqlens",
             "sigattn_valid_flops", "sigattn_worklist_host", "sigattn_last_error", "sigattn_version",
             "sigattn_launch_count", "sigattn_set_profile_events", "sigattn_set_trace_buffer",
-            "sigattn_set_debug_counters", "sigattn_mask_to_index", "sigattn_permute_rows"]
+            "sigattn_set_debug_counters", "sigattn_mask_to_index", "sigattn_permute_rows",
+            "sigattn_fwd_cp", "sigattn_bwd_cp", "sigattn_bwd_cp_workspace_bytes", "sigattn_cp_finalize",
+            "sigattn_ipc_handle_bytes", "sigattn_ipc_export", "sigattn_ipc_import", "sigattn_ipc_close"]
 
 
 class SigattnParams(ctypes.Structure):
@@ -39,6 +41,10 @@ class SigattnParams(ctypes.Structure):
         ("bias_per_seq", ctypes.c_void_p), ("flags", ctypes.c_uint),
         ("dbias", ctypes.c_void_p),
     ]
+
+
+class SigattnCpParams(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int), ("rank", ctypes.c_int), ("peer_acc", ctypes.c_void_p)]
 
 
 class SigattnError(RuntimeError):
@@ -94,6 +100,24 @@ def load():
         lib.sigattn_permute_rows.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, vp]
         lib.sigattn_permute_rows.restype = ctypes.c_int
+    if hasattr(lib, "sigattn_fwd_cp"):
+        CP = ctypes.POINTER(SigattnCpParams)
+        lib.sigattn_fwd_cp.argtypes = [P, CP, vp, vp, vp, vp, ctypes.c_size_t, vp]
+        lib.sigattn_fwd_cp.restype = ctypes.c_int
+        lib.sigattn_bwd_cp.argtypes = [P, CP, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
+        lib.sigattn_bwd_cp.restype = ctypes.c_int
+        lib.sigattn_bwd_cp_workspace_bytes.argtypes = [P]
+        lib.sigattn_bwd_cp_workspace_bytes.restype = ctypes.c_size_t
+        lib.sigattn_cp_finalize.argtypes = [P, ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        lib.sigattn_cp_finalize.restype = ctypes.c_int
+        lib.sigattn_ipc_handle_bytes.argtypes = []
+        lib.sigattn_ipc_handle_bytes.restype = ctypes.c_size_t
+        lib.sigattn_ipc_export.argtypes = [vp, vp]
+        lib.sigattn_ipc_export.restype = ctypes.c_int
+        lib.sigattn_ipc_import.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
+        lib.sigattn_ipc_import.restype = ctypes.c_int
+        lib.sigattn_ipc_close.argtypes = [vp]
+        lib.sigattn_ipc_close.restype = ctypes.c_int
     lib.sigattn_last_error.restype = ctypes.c_char_p
     lib.sigattn_version.restype = ctypes.c_char_p
     _lib = lib

@@ -368,3 +368,103 @@ def sigmoid_attention(q, k, v, seqlens_q=None, seqlens_k=None, key_padding_mask=
     if sk is None and sq is not None and q.shape[ndim] == k.shape[ndim]:
         sk = sq
     return SigmoidAttentionFn.apply(q, k, v, sq, sk, scale, bias, deterministic, layout)
+
+
+# ------------------------------------------------------------------------------------------------
+# key-split context parallelism with the reduction fused into the kernels (include/sigattn.h,
+# sigattn_fwd_cp / sigattn_bwd_cp / sigattn_cp_finalize; A4).  peer_table: int64 CUDA tensor
+# [world] of device pointers to every rank's fp32 accumulator [B, H, Nq / world, d] (see
+# parallel.PeerAccumulators); the orchestration (zeroing, cross-rank ordering) is the caller's.
+def _cp_params(world: int, rank: int, peer_table: torch.Tensor, device):
+    if peer_table.dtype != torch.int64 or peer_table.numel() != world or not peer_table.is_cuda \
+            or peer_table.device != device:
+        raise ValueError("sigattn: peer_table must be an int64 CUDA tensor of `world` device pointers on the "
+                         "inputs' device")
+    return _lib.SigattnCpParams(int(world), int(rank), peer_table.data_ptr())
+
+
+def sigattn_fwd_cp(q, k, v, seqlens_q, seqlens_k, scale, bias: float, peer_table: torch.Tensor, world: int,
+                   rank: int, workspace: Optional[torch.Tensor] = None):
+    """Partial forward over this rank's key block, reduce-added into the owners' accumulators.
+    q: all queries [B, H, Nq, d]; k, v: this rank's block [B, H, Nk, d]; bias: the GLOBAL scalar b."""
+    lib = _lib.load()
+    B, H, Nq, Nk, d = _check_qkv(q, k, v, "bhsd")
+    sq = _lens(seqlens_q, B, q.device)
+    sk = _lens(seqlens_k, B, q.device)
+    p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), float(scale), float(bias), None, 0)
+    cp = _cp_params(world, rank, peer_table, q.device)
+    need = int(lib.sigattn_fwd_workspace_bytes(ctypes.byref(p)))
+    workspace = _workspace(workspace, need, q.device)
+    _lib.check(lib.sigattn_fwd_cp(ctypes.byref(p), ctypes.byref(cp), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                  workspace.data_ptr(), need, _stream_handle(q.device)))
+
+
+def sigattn_bwd_cp(q, k, v, dout, seqlens_q, seqlens_k, scale, bias: float, peer_table: torch.Tensor, world: int,
+                   rank: int, dk=None, dv=None, workspace: Optional[torch.Tensor] = None):
+    """Backward over this rank's key block: returns (dK, dV) of the block (complete); alpha dS K is
+    reduce-added into the owners' fp32 dQ accumulators.  dout: all queries [B, H, Nq, d]."""
+    lib = _lib.load()
+    B, H, Nq, Nk, d = _check_qkv(q, k, v, "bhsd")
+    if dout.shape != q.shape or dout.dtype != q.dtype or not dout.is_contiguous():
+        raise ValueError("sigattn: dout must match q")
+    sq = _lens(seqlens_q, B, q.device)
+    sk = _lens(seqlens_k, B, q.device)
+    if dk is None:
+        dk = torch.empty_like(k)
+    else:
+        _check_out("dk", dk, k.shape, k.dtype, q.device)
+    if dv is None:
+        dv = torch.empty_like(v)
+    else:
+        _check_out("dv", dv, v.shape, v.dtype, q.device)
+    p = _lib.make_params(B, H, Nq, Nk, d, _dtype_code(q), _ptr(sq), _ptr(sk), float(scale), float(bias), None, 0)
+    cp = _cp_params(world, rank, peer_table, q.device)
+    need = int(lib.sigattn_bwd_cp_workspace_bytes(ctypes.byref(p)))
+    workspace = _workspace(workspace, need, q.device)
+    _lib.check(lib.sigattn_bwd_cp(ctypes.byref(p), ctypes.byref(cp), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                  dout.data_ptr(), dk.data_ptr(), dv.data_ptr(), workspace.data_ptr(), need,
+                                  _stream_handle(q.device)))
+    return dk, dv
+
+
+def sigattn_cp_finalize(acc: torch.Tensor, seqlens_q, Nq: int, world: int, rank: int, dtype=torch.bfloat16,
+                        out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """This rank's complete fp32 accumulator [B, H, Nq / world, d] -> [B, H, Nq / world, d] in dtype,
+    rows past the global valid length exact 0."""
+    lib = _lib.load()
+    if acc.dtype != torch.float32 or acc.dim() != 4 or not acc.is_contiguous() or not acc.is_cuda:
+        raise ValueError("sigattn: acc must be a contiguous fp32 CUDA tensor [B, H, Nq / world, d]")
+    B, H, rows, d = acc.shape
+    if rows * world != Nq:
+        raise ValueError("sigattn: acc rows must be Nq / world")
+    sq = _lens(seqlens_q, B, acc.device)
+    if out is None:
+        out = torch.empty(acc.shape, dtype=dtype, device=acc.device)
+    else:
+        _check_out("out", out, acc.shape, dtype, acc.device)
+    code = _lib.SIGATTN_BF16 if dtype == torch.bfloat16 else _lib.SIGATTN_FP16
+    p = _lib.make_params(B, H, Nq, Nq, d, code, _ptr(sq), None, 1.0, 0.0, None, 0)
+    _lib.check(lib.sigattn_cp_finalize(ctypes.byref(p), int(world), int(rank), acc.data_ptr(), out.data_ptr(),
+                                       _stream_handle(acc.device)))
+    return out
+
+
+def ipc_export(t: torch.Tensor) -> bytes:
+    """CUDA IPC handle (plus offset) of a device tensor's memory, for another process's ipc_import."""
+    lib = _lib.load()
+    n = int(lib.sigattn_ipc_handle_bytes())
+    buf = ctypes.create_string_buffer(n)
+    _lib.check(lib.sigattn_ipc_export(t.data_ptr(), buf))
+    return buf.raw
+
+
+def ipc_import(handle: bytes) -> int:
+    """Maps another process's exported buffer on the current device; returns the device pointer."""
+    lib = _lib.load()
+    ptr = ctypes.c_void_p()
+    _lib.check(lib.sigattn_ipc_import(ctypes.c_char_p(handle), ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _lib.check(_lib.load().sigattn_ipc_close(ctypes.c_void_p(ptr)))

@@ -93,7 +93,28 @@ struct BwdArgs {
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots (8 events x 512 tiles)
   int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
   unsigned long long* counters;   // skip accounting (sigattn_set_debug_counters) or nullptr
+  // key-split context parallelism with the dQ reduction fused into the epilogue (sigattn_bwd_cp):
+  // peer_dq[g] is rank g's fp32 accumulator [B, H, peer_rows, D]; alpha dS K of query q is
+  // reduce-added into peer_dq[q / peer_rows] at row q % peer_rows instead of into dq_acc
+  float* const* peer_dq;
+  int peer_rows;
 };
+
+// A staged fp32 dQ tile (n_boxes SW128 boxes of [box_rows][32 floats], 16-byte chunk c of row r at
+// slot c ^ (r & 7)) -> reduce-adds into the owning ranks' accumulators, 8 threads per 128-byte box
+// row so every warp writes 4 full rows (context parallelism, A4: P:121).  tid in [0, 128).
+__device__ __forceinline__ void peer_red_staged(const BwdArgs& args, const uint8_t* tile, int n_boxes, int box_rows,
+                                                int D, int zh, int row0, int nq, uint32_t tid) {
+  for (int hh = 0; hh < n_boxes; ++hh)
+    for (int idx = (int)tid; idx < box_rows * 8; idx += 128) {
+      const int r = idx >> 3, c = idx & 7, qrow = row0 + r;
+      if (qrow >= nq) continue;   // padded query rows carry exact zeros (dS = 0)
+      const float4 v = *reinterpret_cast<const float4*>(tile + hh * box_rows * 128 + r * 128 + ((c ^ (r & 7)) * 16));
+      const int owner = qrow / args.peer_rows, lr = qrow - owner * args.peer_rows;
+      float* dst = args.peer_dq[owner] + ((size_t)zh * args.peer_rows + lr) * D + hh * 32 + c * 4;
+      sm100::red_add_v4_sys(dst, v.x, v.y, v.z, v.w);
+    }
+}
 
 template <int D>
 struct BwdCfg {
@@ -523,7 +544,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     // buffer instead put the reduce's smem read on the dS staging path: +2000 clk per tile.)
     constexpr uint32_t kEpiThread0 = 32 * kComputeWarps;
 #define EPI_TR(tt, e) if (threadIdx.x == kEpiThread0 && (tt) >= 40 && (tt) < 48) sm100::trace_event(args.trace, 3072 + ((tt) - 40) * 16 + (e), 4094)
-    auto drain_dq = [&](uint32_t tq, int zh, int i) {
+    auto drain_dq = [&](uint32_t tq, int zh, int i, int nq_) {
       sm100::mbar_wait(dq_full, tq & 1);
       EPI_TR(tq + 1, 7);
       sm100::tc_fence_after();
@@ -560,7 +581,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::fence_proxy_async_smem();
       sm100::named_bar_sync(1, 128);
       EPI_TR(tq + 1, 9);
-      if (threadIdx.x == kEpiThread0 && !SIGATTN_DBG_NORED) {
+      if (args.peer_dq) {
+        peer_red_staged(args, buf, 2, kTile, D, zh, i * kTile, nq_, threadIdx.x - kEpiThread0);
+      } else if (threadIdx.x == kEpiThread0 && !SIGATTN_DBG_NORED) {
         // rows past Nq are clipped by the TMA; padded query rows add exact zeros (dS = 0 there)
         sm100::tma_reduce_add_3d(&tmDQ, buf, 0, i * kTile, zh);
         sm100::tma_reduce_add_3d(&tmDQ, buf + kTile * 128, 32, i * kTile, zh);
@@ -570,7 +593,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     };
     uint32_t t = 0, item_c = 0;
     bool pend = false;            // a dQ tile waiting to be drained
-    int pend_zh = 0, pend_i = 0;
+    int pend_zh = 0, pend_i = 0, pend_nq = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
@@ -609,10 +632,11 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           }
           EPI_TR(t, qh == 0 ? 3 : 6);
         }
-        if (pend) drain_dq(t - 1, pend_zh, pend_i);
+        if (pend) drain_dq(t - 1, pend_zh, pend_i, pend_nq);
         pend = true;
         pend_zh = (int)zh;
         pend_i = i;
+        pend_nq = nq;
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
       sm100::mbar_wait_backoff(acc_full, item_c & 1);
@@ -658,7 +682,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       ++item_c;
     }
-    if (kDQ && pend) drain_dq(t - 1, pend_zh, pend_i);
+    if (kDQ && pend) drain_dq(t - 1, pend_zh, pend_i, pend_nq);
+    if (kDQ && args.peer_dq) sm100::fence_sys();   // peer reductions before kernel completion
     if (kDQ && threadIdx.x == kEpiThread0) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
   }
 

@@ -56,7 +56,24 @@ struct FwdArgs {
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots
   int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
   unsigned long long* counters;   // skip accounting (sigattn_set_debug_counters) or nullptr
+  // key-split context parallelism with the reduction fused into the epilogue (sigattn_fwd_cp):
+  // peer_o[g] is rank g's fp32 accumulator [B, H, peer_rows, D] (peer_rows = Nq / world); the
+  // partial O row of query q is reduce-added into peer_o[q / peer_rows] at row q % peer_rows
+  float* const* peer_o;
+  int peer_rows;
 };
+
+// fp32 partial O row -> the owning rank's accumulator (context parallelism, A4: P:121).  32 values
+// of row qrow, columns [c0, c0 + 32).
+__device__ __forceinline__ void peer_red_row32(const FwdArgs& args, int D, int b, int h, int qrow, int c0,
+                                               const uint32_t (&v)[32]) {
+  const int owner = qrow / args.peer_rows, lr = qrow - owner * args.peer_rows;
+  float* dst = args.peer_o[owner] + ((size_t)(b * args.H + h) * args.peer_rows + lr) * D + c0;
+#pragma unroll
+  for (int e = 0; e < 32; e += 4)
+    sm100::red_add_v4_sys(dst + e, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                          __uint_as_float(v[e + 3]));
+}
 
 template <int D>
 struct FwdCfg {
@@ -415,7 +432,9 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&o_empty[ob]);
           }
-          if (qrow < args.Nq) {
+          if (kOutF32 && args.peer_o) {
+            if (valid) peer_red_row32(args, D, b, h, qrow, gp * kPart + h0, ov);
+          } else if (qrow < args.Nq) {
             const size_t off = row_off(args.bshd, args.H, args.Nq, D, b, h, qrow) + gp * kPart + h0;
             if constexpr (kOutF32) {
               float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + off);
@@ -446,10 +465,11 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
   }
 
-  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill)   // padded O rows beyond the last valid tile
+  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill && args.o)   // padded O rows beyond the last valid tile
     pad_fill_warp(args.o, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
                   128, lane, args.bshd, args.fill_pad);
 
+  if (kOutF32 && args.peer_o) sm100::fence_sys();   // this CTA's peer reductions before kernel completion
   sm100::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) sm100::trace_globaltime(args.trace, 4095);

@@ -326,7 +326,9 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&o_empty[x]);
         }
-        if (qrow < args.Nq) {
+        if (kOutF32 && args.peer_o) {
+          if (valid) peer_red_row32(args, D, b, h, qrow, c0, ov);
+        } else if (qrow < args.Nq) {
           if constexpr (kOutF32) {
             float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + rowoff + c0);
 #pragma unroll
@@ -352,10 +354,11 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     }
   }
 
-  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill)   // padded O rows beyond the last valid tile
+  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill && args.o)   // padded O rows beyond the last valid tile
     pad_fill_warp(args.o, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
                   kTile, lane, args.bshd, args.fill_pad);
 
+  if (kOutF32 && args.peer_o) sm100::fence_sys();   // this CTA's peer reductions before kernel completion
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);

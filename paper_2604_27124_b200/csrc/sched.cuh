@@ -243,6 +243,26 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, uint16_t* __re
                             threadIdx.x & 31, bshd ? (size_t)H * D : (size_t)D);
 }
 
+
+// Context-parallel finalize: rank `rank`'s fp32 accumulator [B, H, rows, D] (the sum over every
+// rank's key block, A4 P:121) -> out [B, H, rows, D] 16-bit; local row r is global query row
+// rank * rows + r and is written as exact 0 when that row is padded (>= n_q[b]).
+template <bool kBf16>
+__global__ void cp_finalize_kernel(const float* __restrict__ acc, uint16_t* __restrict__ out, int H, int rows, int D,
+                                   int Nq, const int32_t* __restrict__ lens, int rank) {
+  const int zh = blockIdx.y;
+  const int nq = clamp_len(lens, zh / H, Nq);
+  const int nloc = max(0, min(rows, nq - rank * rows));   // valid rows of this block
+  const int per = (rows + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int wper = (r1 - r0 + nwarps - 1) / nwarps;
+  const int w0 = r0 + warp * wper, w1 = min(r1, w0 + wper);
+  if (w0 < w1)
+    dq_finalize_rows<kBf16>(acc + (size_t)zh * rows * D, out + (size_t)zh * rows * D, D, w0, w1, nloc,
+                            threadIdx.x & 31, (size_t)D);
+}
+
 // General (non-prefix) key_padding_mask [B, N] (1 = pad) -> a stable compaction per sequence:
 // index[b, r] = position of the r-th valid token for r < n_b, then of the (r - n_b)-th padded one;
 // seqlens[b] = n_b.  One CTA of 1024 threads per sequence; chunks of 1024 positions scanned with

@@ -36,6 +36,13 @@ using namespace sigattn;
 namespace {
 
 thread_local std::string g_err;
+
+// Key-split context parallelism with the reduction fused into the kernels' epilogues: the device
+// table of every rank's fp32 accumulator and the rows each rank owns (Nq / world).
+struct CpTarget {
+  float* const* peer;
+  int rows;
+};
 std::atomic<long long> g_launches{0};
 thread_local cudaEvent_t g_prof[4] = {nullptr, nullptr, nullptr, nullptr};
 thread_local long long* g_trace = nullptr;
@@ -215,7 +222,8 @@ sigattn_status launch_bwd_prep(const sigattn_params* p, int4* items, int* n_item
 
 template <int D, bool kBf16, bool kF32>
 sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k, const void* v, void* o,
-                          const int4* items, const int* n_items, int max_items, cudaStream_t s) {
+                          const int4* items, const int* n_items, int max_items, cudaStream_t s,
+                          const CpTarget* cp = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv;
   sigattn_status st;
@@ -239,6 +247,8 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   a.trace = g_trace;
   a.counters = g_counters;
   a.bshd = layout_bshd(p) ? 1 : 0;
+  a.peer_o = cp ? cp->peer : nullptr;
+  a.peer_rows = cp ? cp->rows : 0;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   if constexpr (use_fwd2(D)) {
     using C = Fwd2Cfg<D>;
@@ -263,7 +273,7 @@ template <int D, bool kBf16, bool kDQ = true, bool kDB = false>
 sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                           float* dq_acc, void* dk, void* dv,
                           const int4* items, const int* n_items, int max_items, cudaStream_t s,
-                          void* dq_pad = nullptr) {
+                          void* dq_pad = nullptr, const CpTarget* cp = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
   sigattn_status st;
@@ -273,7 +283,7 @@ sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* 
   if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
   CUtensorMap tdq;   // fp32 dQ accumulator, 32-column boxes for the TMA reduce-add
   std::memset(&tdq, 0, sizeof(tdq));
-  if (kDQ && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, p->B, p->H, false)) != SIGATTN_OK)
+  if (kDQ && !cp && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, p->B, p->H, false)) != SIGATTN_OK)
     return st;
   BwdArgs a;
   a.items = items;
@@ -296,6 +306,8 @@ sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* 
   a.trace = g_trace;
   a.counters = g_counters;
   a.bshd = layout_bshd(p) ? 1 : 0;
+  a.peer_dq = cp ? cp->peer : nullptr;
+  a.peer_rows = cp ? cp->rows : 0;
   using C = BwdCfg<D>;
   auto kern = layout_bshd(p) ? sigattn_bwd_kernel<D, kBf16, kDQ, kDB, true> : sigattn_bwd_kernel<D, kBf16, kDQ, kDB, false>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
@@ -312,7 +324,7 @@ template <bool kBf16, bool kDQ = true, bool kDB = false>
 sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                              float* dq_acc, void* dk, void* dv,
                              const int4* items, const int* n_items, int max_items, cudaStream_t s,
-                             void* dq_pad = nullptr) {
+                             void* dq_pad = nullptr, const CpTarget* cp = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
   sigattn_status st;
@@ -322,8 +334,8 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   if ((st = make_tmap(&tdo, dout, dt, 2, 128, p->Nq, p->B, p->H, layout_bshd(p), Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
   CUtensorMap tdq;   // fp32 dQ accumulator [B, H, Nq, 128], 32-column x 64-row boxes for the TMA reduce-add
   std::memset(&tdq, 0, sizeof(tdq));
-  if (kDQ && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 128, p->Nq, p->B, p->H, false,
-                             Bwd128Cfg::kQT)) != SIGATTN_OK)
+  if (kDQ && !cp && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 128, p->Nq, p->B, p->H, false,
+                                    Bwd128Cfg::kQT)) != SIGATTN_OK)
     return st;
   BwdArgs a;
   a.items = items;
@@ -346,6 +358,8 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   a.trace = g_trace;
   a.counters = g_counters;
   a.bshd = layout_bshd(p) ? 1 : 0;
+  a.peer_dq = cp ? cp->peer : nullptr;
+  a.peer_rows = cp ? cp->rows : 0;
   auto kern = layout_bshd(p) ? sigattn_bwd128_kernel<kBf16, kDQ, kDB, true> : sigattn_bwd128_kernel<kBf16, kDQ, kDB, false>;
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
@@ -361,16 +375,16 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
 template <int D, bool kBf16, bool kDQ = true>
 sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                           float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
-                          cudaStream_t s, void* dq_pad = nullptr) {
-  return p->dbias ? launch_bwd_t<D, kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad)
-                  : launch_bwd_t<D, kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad);
+                          cudaStream_t s, void* dq_pad = nullptr, const CpTarget* cp = nullptr) {
+  return p->dbias ? launch_bwd_t<D, kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad, cp)
+                  : launch_bwd_t<D, kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad, cp);
 }
 template <bool kBf16, bool kDQ = true>
 sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                              float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
-                             cudaStream_t s, void* dq_pad = nullptr) {
-  return p->dbias ? launch_bwd128_t<kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad)
-                  : launch_bwd128_t<kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad);
+                             cudaStream_t s, void* dq_pad = nullptr, const CpTarget* cp = nullptr) {
+  return p->dbias ? launch_bwd128_t<kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad, cp)
+                  : launch_bwd128_t<kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad, cp);
 }
 
 template <int D, bool kBf16, bool kF32>
@@ -664,6 +678,169 @@ sigattn_status sigattn_mask_to_seqlens(const uint8_t* key_padding_mask, int B, i
   mask_to_seqlens_kernel<<<B, 256, 0, s>>>(key_padding_mask, N, seqlens, nonprefix_flag);
   count_launch();
   CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ key-split context parallelism
+// with the partial-sum reduction fused into the kernels (A4)
+
+namespace {
+sigattn_status check_cp(const sigattn_params* p, const sigattn_cp_params* cp) {
+  if (!cp || cp->world < 1 || cp->rank < 0 || cp->rank >= cp->world || !cp->peer_acc)
+    return fail(SIGATTN_EINVAL, "bad sigattn_cp_params");
+  if (p->Nq % cp->world) return fail(SIGATTN_EINVAL, "context parallelism needs Nq divisible by world");
+  if (layout_bshd(p)) return fail(SIGATTN_EUNSUPPORTED, "context parallelism needs the [B, H, N, d] layout");
+  if (!aligned16(cp->peer_acc)) return fail(SIGATTN_EINVAL, "peer_acc must be 16-byte aligned");
+  return SIGATTN_OK;
+}
+}  // namespace
+
+extern "C" {
+
+size_t sigattn_bwd_cp_workspace_bytes(const sigattn_params* p) {
+  if (check_params(p) != SIGATTN_OK) return 0;
+  return ws_items_bytes(p);
+}
+
+sigattn_status sigattn_fwd_cp(const sigattn_params* p, const sigattn_cp_params* cp, const void* q, const void* k,
+                              const void* v, void* workspace, size_t workspace_bytes, void* stream) {
+  sigattn_status st = check_params(p);
+  if (st != SIGATTN_OK) return st;
+  if ((st = check_cp(p, cp)) != SIGATTN_OK) return st;
+  if (!q || !k || !v || !workspace) return fail(SIGATTN_EINVAL, "null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(workspace))
+    return fail(SIGATTN_EINVAL, "pointers must be 16-byte aligned");
+  if (workspace_bytes < ws_fwd_bytes(p))
+    return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(ws_fwd_bytes(p)) + " bytes");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((st = sanitize_pad(p, q, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
+  if ((st = sanitize_pad(p, k, p->Nk, p->seqlens_k, s)) != SIGATTN_OK) return st;
+  if ((st = sanitize_pad(p, v, p->Nk, p->seqlens_k, s)) != SIGATTN_OK) return st;
+  const CpTarget t{cp->peer_acc, p->Nq / cp->world};
+  const int max_items = p->B * p->H * cdiv(p->Nq, 128);
+  int* n_items = reinterpret_cast<int*>(workspace);
+  int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(workspace) + 16);
+  if ((st = launch_worklist(fwd_item_kind(p->d), p, items, n_items, s)) != SIGATTN_OK) return st;
+  const bool bf = p->dtype == SIGATTN_BF16;
+  if (p->d == 64)
+    return bf ? launch_fwd<64, true, true>(p, q, k, v, nullptr, items, n_items, max_items, s, &t)
+              : launch_fwd<64, false, true>(p, q, k, v, nullptr, items, n_items, max_items, s, &t);
+  return bf ? launch_fwd<128, true, true>(p, q, k, v, nullptr, items, n_items, max_items, s, &t)
+            : launch_fwd<128, false, true>(p, q, k, v, nullptr, items, n_items, max_items, s, &t);
+}
+
+sigattn_status sigattn_bwd_cp(const sigattn_params* p, const sigattn_cp_params* cp, const void* q, const void* k,
+                              const void* v, const void* dout, void* dk, void* dv, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  sigattn_status st = check_params(p);
+  if (st != SIGATTN_OK) return st;
+  if ((st = check_cp(p, cp)) != SIGATTN_OK) return st;
+  if (p->flags & SIGATTN_F_BWD_DETERMINISTIC)
+    return fail(SIGATTN_EUNSUPPORTED, "the fused context-parallel backward has no deterministic mode");
+  if (!q || !k || !v || !dout || !dk || !dv || !workspace) return fail(SIGATTN_EINVAL, "null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dk) || !aligned16(dv) ||
+      !aligned16(workspace))
+    return fail(SIGATTN_EINVAL, "pointers must be 16-byte aligned");
+  if (workspace_bytes < ws_items_bytes(p))
+    return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(ws_items_bytes(p)) + " bytes");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((st = sanitize_pad(p, q, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
+  if ((st = sanitize_pad(p, dout, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
+  if ((st = sanitize_pad(p, k, p->Nk, p->seqlens_k, s)) != SIGATTN_OK) return st;
+  if ((st = sanitize_pad(p, v, p->Nk, p->seqlens_k, s)) != SIGATTN_OK) return st;
+  const CpTarget t{cp->peer_acc, p->Nq / cp->world};
+  int* n_items = reinterpret_cast<int*>(workspace);
+  int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(workspace) + 16);
+  const int max_items = p->B * p->H * cdiv(p->Nk, 128);
+  if ((st = launch_bwd_prep(p, items, n_items, nullptr, s)) != SIGATTN_OK) return st;
+  const bool bf = p->dtype == SIGATTN_BF16;
+  if (p->d == 64)
+    return bf ? launch_bwd<64, true>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s, nullptr, &t)
+              : launch_bwd<64, false>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s, nullptr, &t);
+  return bf ? launch_bwd128<true>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s, nullptr, &t)
+            : launch_bwd128<false>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s, nullptr, &t);
+}
+
+sigattn_status sigattn_cp_finalize(const sigattn_params* p, int world, int rank, const float* acc, void* out,
+                                   void* stream) {
+  sigattn_status st = check_params(p);
+  if (st != SIGATTN_OK) return st;
+  if (world < 1 || rank < 0 || rank >= world || p->Nq % world) return fail(SIGATTN_EINVAL, "bad world / rank");
+  if (!acc || !out) return fail(SIGATTN_EINVAL, "null pointer");
+  if (!aligned16(acc) || !aligned16(out)) return fail(SIGATTN_EINVAL, "pointers must be 16-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int rows = p->Nq / world;
+  const dim3 grid(std::max(1, std::min(32, cdiv(rows, 512))), p->B * p->H);
+  if (p->dtype == SIGATTN_BF16)
+    cp_finalize_kernel<true><<<grid, 256, 0, s>>>(acc, reinterpret_cast<uint16_t*>(out), p->H, rows, p->d, p->Nq,
+                                                  p->seqlens_q, rank);
+  else
+    cp_finalize_kernel<false><<<grid, 256, 0, s>>>(acc, reinterpret_cast<uint16_t*>(out), p->H, rows, p->d, p->Nq,
+                                                   p->seqlens_q, rank);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
+}
+
+// CUDA IPC: a handle is the cudaIpcMemHandle_t of the allocation containing the pointer, followed by
+// the pointer's byte offset in it (int64), so interior pointers of a caching allocator's blocks work.
+namespace {
+std::mutex g_ipc_mu;
+std::map<void*, void*> g_ipc_bases;   // imported pointer -> mapped allocation base
+}  // namespace
+
+size_t sigattn_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t) + sizeof(int64_t); }
+
+sigattn_status sigattn_ipc_export(const void* dev_ptr, void* handle) {
+  if (!dev_ptr || !handle) return fail(SIGATTN_EINVAL, "null pointer");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  {
+    cudaPointerAttributes attr;
+    CUDA_TRY(cudaPointerGetAttributes(&attr, dev_ptr));
+    if (attr.type != cudaMemoryTypeDevice) return fail(SIGATTN_EINVAL, "ipc export needs device memory");
+  }
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+  if (!fn) return fail(SIGATTN_ECUDA, "cuMemGetAddressRange unavailable");
+  using F = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  if (reinterpret_cast<F>(fn)(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(SIGATTN_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  const int64_t off = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  std::memcpy(handle, &h, sizeof(h));
+  std::memcpy(reinterpret_cast<uint8_t*>(handle) + sizeof(h), &off, sizeof(off));
+  return SIGATTN_OK;
+}
+
+sigattn_status sigattn_ipc_import(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(SIGATTN_EINVAL, "null pointer");
+  cudaIpcMemHandle_t h;
+  int64_t off;
+  std::memcpy(&h, handle, sizeof(h));
+  std::memcpy(&off, reinterpret_cast<const uint8_t*>(handle) + sizeof(h), sizeof(off));
+  void* base = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr = reinterpret_cast<uint8_t*>(base) + off;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_bases[*dev_ptr] = base;
+  return SIGATTN_OK;
+}
+
+sigattn_status sigattn_ipc_close(void* dev_ptr) {
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto it = g_ipc_bases.find(dev_ptr);
+    if (it == g_ipc_bases.end()) return fail(SIGATTN_EINVAL, "pointer was not imported by sigattn_ipc_import");
+    base = it->second;
+    g_ipc_bases.erase(it);
+  }
+  CUDA_TRY(cudaIpcCloseMemHandle(base));
   return SIGATTN_OK;
 }
 

@@ -474,4 +474,16 @@ __device__ __forceinline__ void setmaxnreg_dec() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
 }
 
+
+// ------------------------------------------------------------------ peer-memory reduction
+// Vector fp32 reduce-add with system scope: the target may be another GPU's memory mapped through
+// CUDA IPC / NVLink (all ranks add into the owner's buffer concurrently; the adds are performed at
+// the owner).  No return value (red, not atom).
+__device__ __forceinline__ void red_add_v4_sys(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
+
 }  // namespace sm100
