@@ -6,9 +6,12 @@
 A "step" is one pass of the whole hot path: forward (work list, zero fill, fwd
 kernel) + backward (work list, zeroing, fused bwd kernel, dQ finalise) over one synthetic C3
 batch (B=32, N=8192, H=12, d=64, CellxGene-like jagged lengths; BASELINE config 3).
-Multi-GPU (torchrun, one process per GPU): every rank runs its own C3 batch (different seed),
-no collective on the data path -> "scaling": "weak"; value = total valid FLOPs of all ranks /
-max-over-ranks time.  Inputs (1.6 GB padded) are larger than the 126 MB L2.
+Multi-GPU (one process per GPU; `--gpus N` outside torchrun re-launches itself under
+torch.distributed.run): every rank runs its own C3 batch (different seed), no collective on the
+data path -> "scaling": "weak"; value = total valid FLOPs of all ranks / max-over-ranks time.
+Inputs (1.6 GB padded) are larger than the 126 MB L2.  --workload c4 (the 160M encoder layer's
+192 (b,h) pairs sharded over the ranks) and c5 (one 16K sequence key-split, --cp fused|nccl) are
+strong-scaling runs of the other BASELINE configs.
 
 --impl reference times the fp64 CPU oracle (oracle/, the only reference this tier has) on a
 bounded sample of the same workload on the box's host cores (rank 0 only).
@@ -44,9 +47,12 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
-    ap.add_argument("--workload", default="c3",
-                    help="c3 (BASELINE metric config, default) | c4 (one 160M-encoder layer: B=16 H=12 N=8192 d=64) | "
-                         "c5 (N=16384 B=1 H=16 d=128) | c2:N:d (fwd+bwd, unpadded)")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c5"],
+                    help="c3 (BASELINE metric config, default; weak scaling) | c4 (one 160M-encoder layer: B=16 H=12 "
+                         "N=8192 d=64, (b,h) pairs sharded: strong scaling) | c5 (N=16384 B=1 H=16 d=128 key-split "
+                         "context parallel: strong scaling)")
+    ap.add_argument("--cp", default="fused", choices=["fused", "nccl"],
+                    help="c5: partial sums reduce-added by the kernels (fused, f1) or NCCL reduce-scatter")
     return ap.parse_args()
 
 
@@ -58,14 +64,15 @@ def load_peaks():
     return 1590.0, 1400.0, "fallback"   # B200_PROFILING.md fallback
 
 
-def load_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def load_traffic(workload):
+    """dram bytes per launch of the backward kernel on this workload, from the committed ncu --set full
+    summary (profiles/ncu_summary.json, keyed by workload); None when that workload was not captured."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if not os.path.exists(p):
+    if not os.path.exists(p) or workload is None:
         return None
     try:
         d = json.load(open(p))
-        return d.get("bwd_kernel", {}).get("dram_bytes_per_launch")
+        return d.get(workload, {}).get("bwd_kernel", {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -158,7 +165,7 @@ def oracle_sample(budget_s: float, seed: int = 1):
     t = run(R)
     flops = 14 * d * n * R
     return {"value": flops / t / 1e12, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
-            "seconds": t, "sample": f"C3 longest sequence (n=8192, d=64) head 0: {R} query rows (O, dQ) + {R} key rows "
+            "cpu_model": cpu_model(), "extrapolated": True, "seconds": t, "sample": f"C3 longest sequence (n=8192, d=64) head 0: {R} query rows (O, dQ) + {R} key rows "
                                     f"(dK, dV) of fp64 oracle = {R}/8192 of one (b,h) fwd+bwd; credited 14*d*n*R FLOPs"}
 
 
@@ -188,6 +195,158 @@ def reference_arm(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- workloads
+class Workload:
+    """One timed step of the hot path on this rank.  total_flops: valid-token FLOPs of the step summed
+    over ALL ranks (fwd 4d + bwd 10d per valid pair, App. B.1); fwd/bwd: this rank's kernel-only
+    FLOPs (for the roofline of the kernels whose launches the library times)."""
+    name = ""
+    scaling = "weak"
+    metric = METRIC
+    rank_fwd_flops = 0
+    rank_bwd_flops = 0
+    total_flops = 0
+    config = {}
+    traffic_key = None
+
+    def step(self):
+        raise NotImplementedError
+
+
+class C3Weak(Workload):
+    """BASELINE config 3 (the metric's config): every rank its own C3 batch (different seed), no
+    collective on the data path -> weak scaling."""
+
+    def __init__(self, dev, rank, world, sa, I):
+        cfg = I.C3
+        self.cfg, self.sa = cfg, sa
+        self.q, self.k, self.v, self.do, self.nq, self.nk = I.make_inputs_gpu_fast(cfg, dev, seed_offset=rank)
+        self.alpha, self.bias = 1.0 / math.sqrt(cfg.d), -math.log(cfg.N)
+        self.o = torch_empty_like(self.q)
+        self.dq, self.dk, self.dv = torch_empty_like(self.q), torch_empty_like(self.k), torch_empty_like(self.v)
+        self.ws = workspace(sa.bwd_workspace_bytes(cfg.B, cfg.H, cfg.N, cfg.N, cfg.d), dev)
+        self.fws = workspace(sa.fwd_workspace_bytes(cfg.B, cfg.H, cfg.N, cfg.N, cfg.d), dev)
+        self.rank_fwd_flops = sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, True)
+        self.rank_bwd_flops = sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, False)
+        self.total_flops = world * (self.rank_fwd_flops + self.rank_bwd_flops)
+        self.name = cfg.name
+        self.traffic_key = "c3"
+        self.config = {"workload": cfg.name, "B": cfg.B, "H": cfg.H, "N": cfg.N, "d": cfg.d,
+                       "lengths": "C3 log-normal (pinned, PCG64 seed 1), 73.6% padding",
+                       "bias": "-log N", "scale": "1/sqrt(d)",
+                       "l2": "inputs larger than L2 (Q,K,V,dO 1.6 GB padded per rank) - no flush",
+                       "parallelism": f"batch-sharded weak scaling: {world} rank(s), each its own C3 batch, "
+                                      "no data-path collective"}
+
+    def step(self):
+        sa = self.sa
+        sa.sigattn_fwd(self.q, self.k, self.v, self.nq, self.nk, self.alpha, self.bias, out=self.o, workspace=self.fws)
+        sa.sigattn_bwd(self.q, self.k, self.v, self.do, self.nq, self.nk, self.alpha, self.bias, dq=self.dq,
+                       dk=self.dk, dv=self.dv, workspace=self.ws)
+
+
+class C4Strong(Workload):
+    """BASELINE config 4: one attention layer of the 160M encoder (B=16, H=12, N=8192, d=64), its
+    192 (b, h) pairs LPT-sharded over the ranks (parallel.shard_pairs) -- heads are independent, no
+    collective -> strong scaling (the total work is fixed)."""
+    scaling = "strong"
+
+    def __init__(self, dev, rank, world, sa, I, par):
+        cfg = I.c4_layer(0)
+        self.sa = sa
+        q, k, v, do, nq, nk = I.make_inputs_gpu_fast(cfg, dev)
+        pairs = par.shard_pairs(cfg.B, cfg.H, cfg.nq, cfg.nk, world)[rank]
+        self.q, self.k, self.v, self.do = (par.gather_pairs(t, pairs) for t in (q, k, v, do))   # at rest: sharded
+        del q, k, v, do
+        lens = [cfg.nq[b] for b, _ in pairs]
+        self.nq = self.nk = torch_tensor_i32(lens, dev)
+        P = len(pairs)
+        self.alpha, self.bias = 1.0 / math.sqrt(cfg.d), -math.log(cfg.N)
+        self.o = torch_empty_like(self.q)
+        self.dq, self.dk, self.dv = torch_empty_like(self.q), torch_empty_like(self.k), torch_empty_like(self.v)
+        self.ws = workspace(sa.bwd_workspace_bytes(P, 1, cfg.N, cfg.N, cfg.d), dev)
+        self.fws = workspace(sa.fwd_workspace_bytes(P, 1, cfg.N, cfg.N, cfg.d), dev)
+        self.rank_fwd_flops = sa.valid_flops(P, 1, cfg.d, lens, lens, True)
+        self.rank_bwd_flops = sa.valid_flops(P, 1, cfg.d, lens, lens, False)
+        self.total_flops = (sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, True)
+                            + sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, False))
+        self.name = cfg.name
+        self.traffic_key = "c4"
+        self.config = {"workload": cfg.name, "B": cfg.B, "H": cfg.H, "N": cfg.N, "d": cfg.d, "lengths": "unpadded",
+                       "bias": "-log N", "scale": "1/sqrt(d)",
+                       "l2": "inputs larger than L2 at world <= 4 (Q,K,V,dO 805 MB total) - no flush",
+                       "parallelism": f"batch x head sharded strong scaling: 192 (b,h) pairs LPT over {world} rank(s), "
+                                      f"{P} on this rank, no data-path collective"}
+
+    step = C3Weak.step
+
+
+class C5ContextParallel(Workload):
+    """BASELINE config 5: one N=16384 sequence (H=16, d=128) key-split over the ranks (A4).
+    fused: partial O / dQ rows reduce-added by the kernels into the owners' accumulators (f1);
+    nccl: fp32 partials + NCCL reduce-scatter.  Q / dO all-gathers included -> strong scaling."""
+    scaling = "strong"
+
+    def __init__(self, dev, rank, world, sa, I, par, mode):
+        cfg = I.c5(16, 128)
+        self.cfg, self.sa, self.par, self.mode, self.world = cfg, sa, par, mode, world
+        q, k, v, do, _, _ = I.make_inputs_gpu_fast(cfg, dev)
+        self.shard = par.CPShard(rank, world, cfg.N)
+        sl = slice(rank * self.shard.block, (rank + 1) * self.shard.block)
+        self.q, self.k, self.v, self.do = (t[:, :, sl].contiguous() for t in (q, k, v, do))
+        del q, k, v, do
+        n = self.shard.block
+        if mode == "fused":
+            self.po = par.PeerAccumulators(cfg.B, cfg.H, n, cfg.d, dev)
+            self.pdq = par.PeerAccumulators(cfg.B, cfg.H, n, cfg.d, dev)
+        self.total_flops = (sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, True)
+                            + sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, False))
+        self.rank_fwd_flops = 4 * cfg.H * cfg.d * cfg.N * n
+        self.rank_bwd_flops = 10 * cfg.H * cfg.d * cfg.N * n
+        self.name = cfg.name + "_" + mode
+        self.traffic_key = "c5"
+        self.config = {"workload": self.name, "B": cfg.B, "H": cfg.H, "N": cfg.N, "d": cfg.d, "lengths": "unpadded",
+                       "bias": "-log N (global N)", "scale": "1/sqrt(d)",
+                       "l2": "per-rank blocks re-read from HBM each step; Q / dO all-gathered every step",
+                       "parallelism": f"key-split context parallel over {world} rank(s) ({n} keys each), "
+                                      + ("partial sums reduce-added by the kernels into the owners' accumulators "
+                                         "(fused, f1)" if mode == "fused" else "fp32 partials + NCCL reduce-scatter")}
+
+    def step(self):
+        par = self.par
+        if self.mode == "fused":
+            o, q_full = par.cp_forward_fused(self.q, self.k, self.v, self.shard, self.po)
+            par.cp_backward_fused(q_full, self.k, self.v, self.do, self.shard, self.pdq)
+        else:
+            o, q_full = par.cp_forward(self.q, self.k, self.v, self.shard)
+            par.cp_backward(q_full, self.k, self.v, self.do, self.shard)
+
+
+def torch_empty_like(t):
+    import torch
+    return torch.empty_like(t)
+
+
+def torch_tensor_i32(x, dev):
+    import torch
+    return torch.tensor(list(x), dtype=torch.int32, device=dev)
+
+
+def workspace(nbytes, dev):
+    import torch
+    return torch.empty(max(1, int(nbytes)), dtype=torch.uint8, device=dev)
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ----------------------------------------------------------------------------- our arm
 def main_ours(args):
     import torch
@@ -196,10 +355,13 @@ def main_ours(args):
     import paper_2604_27124_b200 as sa
     from paper_2604_27124_b200 import _lib
     from paper_2604_27124_b200 import inputs as I
+    from paper_2604_27124_b200 import parallel as par
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -207,34 +369,19 @@ def main_ours(args):
     lib = _lib.load()
 
     if args.workload == "c3":
-        cfg = I.C3
-    elif args.workload == "c5":
-        cfg = I.c5(16, 128)
+        wl = C3Weak(dev, rank, world, sa, I)
     elif args.workload == "c4":
-        cfg = I.c4_layer(0)   # one of the 12 identical-shape attention layers of the 160M encoder
-    elif args.workload.startswith("c2:"):
-        _, n_, d_ = args.workload.split(":")
-        cfg = I.c2(int(n_), int(d_))
+        wl = C4Strong(dev, rank, world, sa, I, par)
+    elif args.workload == "c5":
+        wl = C5ContextParallel(dev, rank, world, sa, I, par, args.cp)
     else:
         raise SystemExit(f"unknown workload {args.workload}")
-    q, k, v, do, nq, nk = I.make_inputs_gpu_fast(cfg, dev, seed_offset=rank)
-    alpha, bias = 1.0 / math.sqrt(cfg.d), -math.log(cfg.N)
-    o = torch.empty_like(q)
-    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    ws = torch.empty(sa.bwd_workspace_bytes(cfg.B, cfg.H, cfg.N, cfg.N, cfg.d), dtype=torch.uint8, device=dev)
-    fws = torch.empty(sa.fwd_workspace_bytes(cfg.B, cfg.H, cfg.N, cfg.N, cfg.d), dtype=torch.uint8, device=dev)
     if args.workload != "c3":
         args.no_e2e = True
         args.no_cpu_baseline = True
-    f_fwd = sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, True)
-    f_bwd = sa.valid_flops(cfg.B, cfg.H, cfg.d, cfg.nq, cfg.nk, False)
-
-    def step():
-        sa.sigattn_fwd(q, k, v, nq, nk, alpha, bias, out=o, workspace=fws)
-        sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, bias, dq=dq, dk=dk, dv=dv, workspace=ws)
 
     for _ in range(max(3, args.warmup)):
-        step()
+        wl.step()
     torch.cuda.synchronize()
 
     K = args.steps
@@ -256,7 +403,7 @@ def main_ours(args):
     for i in range(K):
         marks[i].record()
         lib.sigattn_set_profile_events(*[e.cuda_event for e in ev[i]])
-        step()
+        wl.step()
     marks[K].record()
     stop.record()
     lib.sigattn_set_profile_events(None, None, None, None)
@@ -279,22 +426,22 @@ def main_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, fwd_ms, bwd_ms = (float(x) for x in t.tolist())
     ms_step = ms_total / K
-    flops_step = f_fwd + f_bwd
-    value = world * flops_step / (ms_step * 1e-3) / 1e12
+    value = wl.total_flops / (ms_step * 1e-3) / 1e12
 
-    # ---- end to end through the public API with host (pinned) buffers
+    # ---- end to end through the public API with host (pinned) buffers (C3 only)
     e2e = None
     if not args.no_e2e:
-        hq, hk, hv, hdo = (t_.cpu().pin_memory() for t_ in (q, k, v, do))
-        hnq, hnk = nq.cpu().pin_memory(), nk.cpu().pin_memory()
-        ho, hdq, hdk, hdv = (torch.empty(t_.shape, dtype=t_.dtype, pin_memory=True) for t_ in (q, q, k, v))
+        alpha, bias = wl.alpha, wl.bias
+        hq, hk, hv, hdo = (t_.cpu().pin_memory() for t_ in (wl.q, wl.k, wl.v, wl.do))
+        hnq, hnk = wl.nq.cpu().pin_memory(), wl.nk.cpu().pin_memory()
+        ho, hdq, hdk, hdv = (torch.empty(t_.shape, dtype=t_.dtype, pin_memory=True) for t_ in (wl.q, wl.q, wl.k, wl.v))
 
         def e2e_step():
             dq_, dk_, dv_ = (t_.to(dev, non_blocking=True) for t_ in (hq, hk, hv))
             ddo = hdo.to(dev, non_blocking=True)
             snq, snk = hnq.to(dev, non_blocking=True), hnk.to(dev, non_blocking=True)
-            oo = sa.sigattn_fwd(dq_, dk_, dv_, snq, snk, alpha, bias, workspace=fws)
-            g1, g2, g3 = sa.sigattn_bwd(dq_, dk_, dv_, ddo, snq, snk, alpha, bias, workspace=ws)
+            oo = sa.sigattn_fwd(dq_, dk_, dv_, snq, snk, alpha, bias, workspace=wl.fws)
+            g1, g2, g3 = sa.sigattn_bwd(dq_, dk_, dv_, ddo, snq, snk, alpha, bias, workspace=wl.ws)
             ho.copy_(oo, non_blocking=True)
             hdq.copy_(g1, non_blocking=True)
             hdk.copy_(g2, non_blocking=True)
@@ -315,22 +462,25 @@ def main_ours(args):
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         h2d = sum(t_.numel() * t_.element_size() for t_ in (hq, hk, hv, hdo, hnq, hnk))
         d2h = sum(t_.numel() * t_.element_size() for t_ in (ho, hdq, hdk, hdv))
-        e2e = {"value": world * flops_step / (float(e_ms.item()) * 1e-3) / 1e12, "unit": UNIT,
+        e2e = {"value": wl.total_flops / (float(e_ms.item()) * 1e-3) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(e_ms.item()), "steps": args.e2e_steps,
                "path": "pinned host -> sigattn_fwd/sigattn_bwd (public API) -> pinned host, O and dQ/dK/dV read back"}
 
     peak, peak_sus, peak_src = load_peaks()
-    bwd_tflops = f_bwd / (bwd_ms * 1e-3) / 1e12
-    fwd_tflops = f_fwd / (fwd_ms * 1e-3) / 1e12
-    traffic = load_traffic()
-    roof = {"bound": "tensor", "kernel": f"sigattn_bwd kernel d={cfg.d} bf16 (fused Alg. 2+3)",
+    bwd_tflops = wl.rank_bwd_flops / (bwd_ms * 1e-3) / 1e12
+    fwd_tflops = wl.rank_fwd_flops / (fwd_ms * 1e-3) / 1e12
+    traffic = load_traffic(wl.traffic_key)
+    roof = {"bound": "tensor", "kernel": f"sigattn_bwd kernel d={wl.config['d']} bf16 (fused Alg. 2+3)",
             "achieved": bwd_tflops, "peak": peak, "unit": "TFLOP/s", "frac": bwd_tflops / peak,
-            "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_src}, burst)",
+            "traffic": traffic, "traffic_source": (f"profiles/ncu_summary.json [{wl.traffic_key}]: dram bytes of one "
+                                                   "ncu --set full launch of this kernel on this workload"
+                                                   if traffic is not None else "no ncu capture of this workload"),
+            "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_src}, burst)",
             "frac_of_sustained_peak": bwd_tflops / peak_sus,
-            "algorithmic_flops_per_launch": f_bwd, "avg_launch_ms": bwd_ms,
+            "algorithmic_flops_per_launch": wl.rank_bwd_flops, "avg_launch_ms": bwd_ms,
             "fwd_kernel": {"achieved": fwd_tflops, "frac": fwd_tflops / peak, "avg_launch_ms": fwd_ms,
-                           "algorithmic_flops_per_launch": f_fwd}}
+                           "algorithmic_flops_per_launch": wl.rank_fwd_flops}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -338,15 +488,9 @@ def main_ours(args):
         cpu.pop("seconds", None)
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-                "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": cfg.name, "B": cfg.B, "H": cfg.H, "N": cfg.N, "d": cfg.d,
-                           "lengths": ("C3 log-normal (pinned, PCG64 seed 1), 73.6% padding" if args.workload == "c3"
-                                       else "unpadded"),
-                           "bias": "-log N", "scale": "1/sqrt(d)",
-                           "l2": "inputs larger than L2 (Q,K,V,dO 1.6 GB padded, 0.43 GB valid) - no flush",
-                           "parallelism": f"batch-sharded weak scaling, {world} rank(s), no data-path collective"},
+        line = {"metric": wl.metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+                "ms_per_step": ms_step, "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None,
+                "dtype": "bf16", "data": "synthetic", "config": wl.config,
                 "pct_of_peak": 100.0 * value / world / peak,
                 "pct_of_sustained_peak": 100.0 * value / world / peak_sus,
                 "fwd_tflops": fwd_tflops, "bwd_tflops": bwd_tflops, "fwd_kernel_ms": fwd_ms, "bwd_kernel_ms": bwd_ms,
@@ -355,13 +499,30 @@ def main_ours(args):
                 "context": {"paper_h100_fwd_tflops": PAPER_H100_FWD_TFLOPS,
                             "note": "paper number is H100 fwd-only N=16K d=128; not this workload"}}
         print(json.dumps(line), flush=True)
+    if args.workload == "c5" and args.cp == "fused":
+        wl.po.close()
+        wl.pdq.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
+def relaunch_distributed(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-run this script under torch.distributed.run with
+    N local ranks (127.0.0.1 rendezvous), the contract's launch."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     if args.impl == "reference":
         return reference_arm(args)
     return main_ours(args)

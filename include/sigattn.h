@@ -182,8 +182,11 @@ void sigattn_set_debug_counters(void* device_counters);
  * so G ranks that each hold one key block need no log-sum-exp merge -- only a sum.  Rank g owns
  * query rows [g Nq/G, (g+1) Nq/G) and an fp32 accumulator [B, H, Nq/G, d] for them.  The fused
  * calls below reduce-add (red.global.add.v4.f32, system scope) every partial row straight into the
- * owner's accumulator from the kernel epilogue -- over NVLink when the owner is another GPU --
- * instead of materialising a partial [B, H, Nq, d] tensor and reduce-scattering it afterwards.
+ * owner's accumulator -- over NVLink when the owner is another GPU -- instead of materialising a
+ * partial tensor and reduce-scattering it with a separate collective: the forward straight from the
+ * kernel epilogue (each O row is final for this rank's keys once its query tile's key loop ends),
+ * the backward from a push kernel after the key-tile pass (every key tile adds a dQ partial, which
+ * is summed in L2 first so that each row crosses NVLink once).
  *
  * Per-rank problem in sigattn_params: Nq = the full query length (all queries, e.g. all-gathered
  * Q), Nk = this rank's key block length, seqlens_q = global valid lengths, seqlens_k = the valid
@@ -205,11 +208,11 @@ typedef struct {
 sigattn_status sigattn_fwd_cp(const sigattn_params* p, const sigattn_cp_params* cp, const void* q,
                               const void* k, const void* v, void* workspace, size_t workspace_bytes,
                               void* stream);
-/* Bytes of workspace sigattn_bwd_cp needs (the scheduling area only: dQ goes to the peers).      */
+/* Bytes of workspace sigattn_bwd_cp needs (a local fp32 dQ partial [B, H, Nq, d] + scheduling).  */
 size_t sigattn_bwd_cp_workspace_bytes(const sigattn_params* p);
 /* Backward over this rank's keys: dk, dv [B, H, Nk, d] of this rank's block are complete on return
- * (keys are owned; padded rows 0 as in sigattn_bwd); alpha dS K of every valid query row is
- * reduce-added into the owners' fp32 dQ accumulators.  dout is the full [B, H, Nq, d].            */
+ * (keys are owned; padded rows 0 as in sigattn_bwd); alpha dS K summed over this rank's key tiles is
+ * reduce-added, row by row, into the owners' fp32 dQ accumulators.  dout is the full [B, H, Nq, d]. */
 sigattn_status sigattn_bwd_cp(const sigattn_params* p, const sigattn_cp_params* cp, const void* q,
                               const void* k, const void* v, const void* dout, void* dk, void* dv,
                               void* workspace, size_t workspace_bytes, void* stream);

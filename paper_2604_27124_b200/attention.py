@@ -401,8 +401,9 @@ def sigattn_fwd_cp(q, k, v, seqlens_q, seqlens_k, scale, bias: float, peer_table
 
 def sigattn_bwd_cp(q, k, v, dout, seqlens_q, seqlens_k, scale, bias: float, peer_table: torch.Tensor, world: int,
                    rank: int, dk=None, dv=None, workspace: Optional[torch.Tensor] = None):
-    """Backward over this rank's key block: returns (dK, dV) of the block (complete); alpha dS K is
-    reduce-added into the owners' fp32 dQ accumulators.  dout: all queries [B, H, Nq, d]."""
+    """Backward over this rank's key block: returns (dK, dV) of the block (complete); alpha dS K, summed
+    over this rank's key tiles, is reduce-added into the owners' fp32 dQ accumulators by the library's
+    push kernel.  dout: all queries [B, H, Nq, d]."""
     lib = _lib.load()
     B, H, Nq, Nk, d = _check_qkv(q, k, v, "bhsd")
     if dout.shape != q.shape or dout.dtype != q.dtype or not dout.is_contiguous():

@@ -14,21 +14,19 @@
 // applied once in the epilogues.  sigma is evaluated once per element; the tensor work is the
 // credited 10 d per (query, key) pair.
 //
-// Pipelining: two MMA issuers.  Warp 21 issues S,dP(i, q) as soon as dV/dK(i-1, q) have read the
-// previous tile's P^T/dS^T out of those TMEM columns; warp 22 issues dV/dK(i, q) once the compute warps
-// stored P^T/dS^T(i, q), then dQ(i).  While the compute warps work on one half, the tensor core finishes
-// the other half and prepares the next tile's scores for it.
+// Pipelining: the MMA warp issues, per tile i,   dV/dK(i, q0) | S,dP(i+1, q0) | dV/dK(i, q1) |
+// S,dP(i+1, q1) | dQ(i)   so while the compute warps work on one half, the tensor core finishes the
+// other half and prepares the next tile's scores for it.
 //
 // CTA roles (768 threads, persistent, one CTA per SM; single-thread roles in the highest warp ids,
 // which the warp scheduler favours):
 //   warps 0-15  compute: thread = key row (TMEM lane); all 16 warps process query half 0, then half 1;
 //               warpgroup w takes 16 queries [64q + 16w, +16) of half q
-//   warps 16-19 epilogue warpgroup: dS^T staging into shared memory for the dQ MMA, dQ_i drain
-//               (tcgen05.ld -> x alpha -> swizzled fp32 smem tile -> TMA bulk reduce-add into the
-//               fp32 workspace), dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
+//   warps 16-19 epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
+//               dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
 //   warp 20     TMA: K_j, V_j (2 slots), Q_i + dO_i (3 stages)
-//   warp 21     score MMA issuer (one elected thread); also tcgen05.cp of K_j, V_j into TMEM
-//   warp 22     TMEM allocator, then gradient MMA issuer (dV, dK, dQ)
+//   warp 21     MMA issuer (one elected thread); also tcgen05.cp of K_j, V_j into TMEM
+//   warp 22     TMEM allocator
 // TMEM (d = 64): S^T [0,128) dP^T [128,256) dV [256,320) dK [320,384) dQ [384,448) K [448,480) V [480,512)
 // P^T / dS^T (16-bit) overwrite the first half of each warpgroup's own S^T / dP^T columns.
 // Shared memory: dS^T (16-bit, 128B-swizzled, keys as rows, double-buffered) is read MN-major as
@@ -38,7 +36,7 @@
 #include "sigmoid.cuh"
 
 #ifndef SIGATTN_BWD_MMA_SPIN
-#define SIGATTN_BWD_MMA_SPIN 0    // 1: the gradient-MMA warp spins (no nanosleep back-off) on p_full
+#define SIGATTN_BWD_MMA_SPIN 0    // 1: the MMA warp spins (no nanosleep back-off) on p_full
 #endif
 #if SIGATTN_BWD_MMA_SPIN
 #define MMA_WAIT_P(b, p) sm100::mbar_wait(b, p)
@@ -93,28 +91,7 @@ struct BwdArgs {
   long long* trace;       // SIGATTN_TRACE builds: [grid][4096] clock64 event slots (8 events x 512 tiles)
   int bshd;               // 1: tensors are [B, N, H, d], else [B, H, N, d]
   unsigned long long* counters;   // skip accounting (sigattn_set_debug_counters) or nullptr
-  // key-split context parallelism with the dQ reduction fused into the epilogue (sigattn_bwd_cp):
-  // peer_dq[g] is rank g's fp32 accumulator [B, H, peer_rows, D]; alpha dS K of query q is
-  // reduce-added into peer_dq[q / peer_rows] at row q % peer_rows instead of into dq_acc
-  float* const* peer_dq;
-  int peer_rows;
 };
-
-// A staged fp32 dQ tile (n_boxes SW128 boxes of [box_rows][32 floats], 16-byte chunk c of row r at
-// slot c ^ (r & 7)) -> reduce-adds into the owning ranks' accumulators, 8 threads per 128-byte box
-// row so every warp writes 4 full rows (context parallelism, A4: P:121).  tid in [0, 128).
-__device__ __forceinline__ void peer_red_staged(const BwdArgs& args, const uint8_t* tile, int n_boxes, int box_rows,
-                                                int D, int zh, int row0, int nq, uint32_t tid) {
-  for (int hh = 0; hh < n_boxes; ++hh)
-    for (int idx = (int)tid; idx < box_rows * 8; idx += 128) {
-      const int r = idx >> 3, c = idx & 7, qrow = row0 + r;
-      if (qrow >= nq) continue;   // padded query rows carry exact zeros (dS = 0)
-      const float4 v = *reinterpret_cast<const float4*>(tile + hh * box_rows * 128 + r * 128 + ((c ^ (r & 7)) * 16));
-      const int owner = qrow / args.peer_rows, lr = qrow - owner * args.peer_rows;
-      float* dst = args.peer_dq[owner] + ((size_t)zh * args.peer_rows + lr) * D + hh * 32 + c * 4;
-      sm100::red_add_v4_sys(dst, v.x, v.y, v.z, v.w);
-    }
-}
 
 template <int D>
 struct BwdCfg {
@@ -129,13 +106,11 @@ struct BwdCfg {
   static constexpr int kDSBytes = 2 * kTile * 128;
   static constexpr int kDQOff = kDSOff + 2 * kDSBytes;      // fp32 dQ staging tile for the TMA reduce-add
   static constexpr int kBarOff = kDQOff + kTile * D * 4;
-  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 2 + 1 + 1 + 2 + 2 + 2;
+  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 2 + 1 + 1 + 2 + 2;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kNumWG = 4;                           // compute warpgroups
-  // kWarpMMA issues the score MMAs (S^T, dP^T) and the K/V TMEM copies, kWarpGrad the gradient MMAs
-  // (dV, dK, dQ); kWarpGrad also allocates TMEM before the roles start
   static constexpr int kWarpEpi = 4 * kNumWG, kWarpTMA = kWarpEpi + 4, kWarpMMA = kWarpTMA + 1,
-                       kWarpGrad = kWarpTMA + 2, kWarpAlloc = kWarpTMA + 2, kWarpFill = kWarpTMA + 3;
+                       kWarpAlloc = kWarpTMA + 2, kWarpFill = kWarpTMA + 3;
   static constexpr int kThreads = 32 * (kWarpEpi + 8);
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 320, kColDQ = 384, kColK = 448,
@@ -272,7 +247,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* acc_empty = acc_full + 1;
   uint64_t* ds_copied = acc_empty + 1;            // [2] per query half: epilogue read dS^T from TMEM
   uint64_t* ds_full = ds_copied + 2;              // [2] per dS smem buffer: both halves staged + fenced
-  uint64_t* dvdk_done = ds_full + 2;              // [2] per query half: dV/dK MMAs have read P^T / dS^T
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -288,11 +262,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&p_full[i], kComputeWarps);       // every compute warp works on every half
       sm100::mbar_init(&ds_copied[i], 4);
       sm100::mbar_init(&ds_full[i], 4);                  // the 4 epilogue warps, after both halves
-      sm100::mbar_init(&dvdk_done[i], 1);
     }
     for (int i = 0; i < C::kQStages; ++i) {
       sm100::mbar_init(&qdo_full[i], 1);
-      sm100::mbar_init(&qdo_empty[i], 2);                // both MMA warps read Q_i, dO_i
+      sm100::mbar_init(&qdo_empty[i], 1);
     }
     sm100::mbar_init(dq_full, 1);
     sm100::mbar_init(dq_empty, 4);
@@ -348,13 +321,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       ++kv_c;
     }
-  } else if (warp == C::kWarpMMA || warp == C::kWarpGrad) {
-    // ===================== MMA issuers (whole warp waits, one elected lane issues) =====================
-    // A tcgen05.mma issue blocks while the tensor pipe is busy (the queue holds about one MMA), so an
-    // issuer's barrier waits (~100 clk each, even when already complete) drain the pipe.  Two issuers
-    // whose streams only meet through barriers keep it fed while either one waits:
-    //   kWarpMMA   per tile i, half q: S^T, dP^T(i, q)     (after dV/dK(i-1, q) read P^T/dS^T there)
-    //   kWarpGrad  per tile i: dV, dK(i, q0), dV, dK(i, q1), then dQ(i) = dS(i) K
+  } else if (warp == C::kWarpMMA) {
+    // ===================== MMA issuer (whole warp waits, one elected lane issues) =====================
     constexpr uint32_t idesc_s = sm100::make_idesc_f16(kBf16, 128, 64, false, false);    // S^T_q, dP^T_q
     constexpr uint32_t idesc_acc = sm100::make_idesc_f16(kBf16, 128, D, false, true);    // dV, dK
     constexpr uint32_t idesc_dq = sm100::make_idesc_f16(kBf16, 128, D, true, true);      // dQ
@@ -363,111 +331,166 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
     const uint32_t do_base = sm100::smem_u32(smem + C::kDOOff);
     const uint32_t ds_base = sm100::smem_u32(smem + C::kDSOff);
+
+    // K_j, V_j (smem, SW128 K-major) -> TMEM A-operand layout (16 elements per 8 columns)
+    auto copy_kv = [&](uint32_t kvb) {
+      const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        sm100::tmem_cp_128x256b(tmem + C::kColK + kk * 8, sm100::sdesc_add(sm100::make_sdesc_sw128(ka, 16, 1024), kk * 32));
+        sm100::tmem_cp_128x256b(tmem + C::kColV + kk * 8, sm100::sdesc_add(sm100::make_sdesc_sw128(va, 16, 1024), kk * 32));
+      }
+    };
+    // S^T_q = K Q_q^T and dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; A from TMEM)
+    auto mma1 = [&](uint32_t kvb, uint32_t st, uint32_t q) {
+      const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+      (void)kvb;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+        sm100::mma_ts(tmem + C::kColS + q * 64, tmem + C::kColK + kk * 8,
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(qa, 16, 1024), kk * 32), idesc_s, kk > 0);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+        sm100::mma_ts(tmem + C::kColDP + q * 64, tmem + C::kColV + kk * 8,
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(da, 16, 1024), kk * 32), idesc_s, kk > 0);
+      sm100::mma_commit(&s_full[q]);
+    };
+    // dV += P^T_q dO_q ; dK += dS^T_q Q_q   (M = keys, N = d, K = 64 queries; A from TMEM)
+    auto mma2 = [&](uint32_t st, uint32_t q, bool first) {
+      const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        // queries [64q + 16kk, +16): warpgroup kk packed them at S cols 64q + 16kk + [0, 8)
+        const uint32_t a_col = q * 64 + kk * 16;
+        sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + a_col,
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(da, kTile * 128, 1024), kk * 2048), idesc_acc,
+                      (first && kk == 0) ? 0u : 1u);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t a_col = q * 64 + kk * 16;
+        sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + a_col,
+                      sm100::sdesc_add(sm100::make_sdesc_sw128(qa, kTile * 128, 1024), kk * 2048), idesc_acc,
+                      (first && kk == 0) ? 0u : 1u);
+      }
+    };
+
     TileIter cur;
     cur.init(args.items, n_items);
-    if (warp == C::kWarpMMA) {
-      for (uint32_t t = 0; cur.valid; cur.advance(args.items), ++t) {
-        const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1;
-        if (cur.i == 0) sm100::mbar_wait(&kv_full[kvb], (cur.item_c >> 1) & 1);
-        sm100::mbar_wait(&qdo_full[st], (t / C::kQStages) & 1);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          if (t > 0) {   // the previous tile's P^T / dS^T in these columns are consumed
-            sm100::mbar_wait(&dvdk_done[q], (t - 1) & 1);
-            if (kDQ && !SIGATTN_DBG_MMAONLY) sm100::mbar_wait(&ds_copied[q], (t - 1) & 1);
-          }
-          sm100::tc_fence_after();
-          if (sm100::elect_one()) {
-            if (q == 0 && cur.i == 0) {
-              // K_j, V_j (smem, SW128 K-major) -> TMEM A-operand layout (16 elements per 8 columns); in
-              // order after this warp's last S^T / dP^T MMAs of the previous item, which read them
-              const uint32_t ka = k_base + kvb * C::kTileBytes, va = v_base + kvb * C::kTileBytes;
-#pragma unroll
-              for (int kk = 0; kk < D / 16; ++kk) {
-                sm100::tmem_cp_128x256b(tmem + C::kColK + kk * 8, sm100::sdesc_add(sm100::make_sdesc_sw128(ka, 16, 1024), kk * 32));
-                sm100::tmem_cp_128x256b(tmem + C::kColV + kk * 8, sm100::sdesc_add(sm100::make_sdesc_sw128(va, 16, 1024), kk * 32));
-              }
-            }
-            // S^T_q = K Q_q^T and dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; A from TMEM)
-            const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
-            const uint64_t dq0 = sm100::make_sdesc_sw128(qa, 16, 1024), dd0 = sm100::make_sdesc_sw128(da, 16, 1024);
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              sm100::mma_ts(tmem + C::kColS + q * 64, tmem + C::kColK + kk * 8, dq0 + ((kk * 32) >> 4), idesc_s, kk > 0);
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              sm100::mma_ts(tmem + C::kColDP + q * 64, tmem + C::kColV + kk * 8, dd0 + ((kk * 32) >> 4), idesc_s, kk > 0);
-            sm100::mma_commit(&s_full[q]);
-            if (q == 1) sm100::mma_commit(&qdo_empty[st]);   // this warp's reads of Q_i, dO_i
-          }
-          __syncwarp();
-          if (lane == 0 && t > 0) sm100::trace_event(args.trace, (q == 0 ? 512 : 3328) + t - 1, q == 0 ? 1024 : 4000);
-        }
+    if (cur.valid) {
+      sm100::mbar_wait(&kv_full[cur.item_c & 1], (cur.item_c >> 1) & 1);
+      sm100::mbar_wait(&qdo_full[0], 0);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        copy_kv(cur.item_c & 1);
+        mma1(cur.item_c & 1, 0, 0);
+        mma1(cur.item_c & 1, 0, 1);
       }
-    } else {
-      for (uint32_t t = 0; cur.valid; cur.advance(args.items), ++t) {
-        const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1;
-        const bool last = cur.i == cur.nqt - 1;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          // dV += P^T_q dO_q ; dK += dS^T_q Q_q   (M = keys, N = d, K = 64 queries; A from TMEM)
-#if !SIGATTN_DBG_MMAONLY
-          MMA_WAIT_P(&p_full[q], t & 1);
-          if (lane == 0) sm100::trace_event(args.trace, q * 1024 + t, q * 1024 + 512);
-          if (q == 0 && cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);   // epilogue read previous dV/dK
-#endif
-          sm100::tc_fence_after();
-          if (sm100::elect_one()) {
-            const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
-            const uint64_t dq0 = sm100::make_sdesc_sw128(qa, kTile * 128, 1024), dd0 = sm100::make_sdesc_sw128(da, kTile * 128, 1024);
-            const bool first = cur.i == 0 && q == 0;
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)   // queries [64q + 16kk, +16): warpgroup kk packed them at cols 64q + 16kk + [0, 8)
-              sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + q * 64 + kk * 16, dd0 + ((kk * 2048) >> 4), idesc_acc,
-                            (first && kk == 0) ? 0u : 1u);
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + q * 64 + kk * 16, dq0 + ((kk * 2048) >> 4), idesc_acc,
-                            (first && kk == 0) ? 0u : 1u);
-            sm100::mma_commit(&dvdk_done[q]);
-            if (q == 1) {
-              sm100::mma_commit(&qdo_empty[st]);                 // this warp's reads of Q_i, dO_i
-              if (last) sm100::mma_commit(acc_full);             // dV, dK of this key tile are final
-              if (cur.i == 0 && args.counters) atomicAdd(args.counters + 1, (unsigned long long)cur.nqt);
-            }
-          }
-          __syncwarp();
-        }
-        if constexpr (kDQ) {
-          // dQ(t) = dS(t) K   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major, B = K MN-major)
-#if !SIGATTN_DBG_MMAONLY
-          sm100::mbar_wait(dq_empty, (t & 1) ^ 1);              // epilogue drained the accumulator
-          sm100::mbar_wait(&ds_full[t & 1], (t >> 1) & 1);      // dS(t) staged in smem, proxy-fenced
-#endif
-          sm100::tc_fence_after();
-          if (sm100::elect_one()) {
-            const uint32_t ka = k_base + kvb * C::kTileBytes;
-            const uint64_t ds0 = sm100::make_sdesc_sw128(ds_base + (t & 1) * C::kDSBytes, kTile * 128, 1024);
-            const uint64_t k0 = sm100::make_sdesc_sw128(ka, kTile * 128, 1024);
-#pragma unroll
-            for (int kk = 0; kk < kTile / 16; ++kk)
-              sm100::mma_ss(tmem + C::kColDQ, ds0 + ((kk * 2048) >> 4), k0 + ((kk * 2048) >> 4), idesc_dq, kk > 0);
-            sm100::mma_commit(&ds_free[t & 1]);
-            sm100::mma_commit(dq_full);
-            if (last) sm100::mma_commit(&kv_empty[kvb]);        // K/V smem slot free
-          }
-          __syncwarp();
-          if (lane == 0) sm100::trace_event(args.trace, 1536 + t, 2048);
-        } else {
-          if (sm100::elect_one() && last) sm100::mma_commit(&kv_empty[kvb]);
-          __syncwarp();
-        }
+      __syncwarp();
+    }
+    // dQ(t) = dS(t) K after both halves' next-tile score MMAs (one tile later, between the halves of
+    // tile t+1, measured slower: 3.03 vs 2.57 ms on C3; a second issuer warp for the gradient MMAs,
+    // 2% slower).
+    uint32_t prev_kvb = 0;
+    bool prev_last = false;      // the tile dQ is pending for was its item's last (frees its K/V slot)
+    auto issue_dq = [&](uint32_t tq) {
+      if constexpr (!kDQ) {
+        if (sm100::elect_one() && prev_last) sm100::mma_commit(&kv_empty[prev_kvb]);   // K/V smem slot free
+        __syncwarp();
+        return;
       }
+      const uint32_t b2 = tq & 1;
+#if !SIGATTN_DBG_MMAONLY
+      sm100::mbar_wait(dq_empty, (tq & 1) ^ 1);                  // epilogue drained the accumulator
+      sm100::mbar_wait(&ds_full[b2], (tq >> 1) & 1);             // dS(tq) staged in smem, proxy-fenced
+#endif
+      if (lane == 0 && tq >= 40 && tq < 48) sm100::trace_event(args.trace, 3328 + (tq - 40) * 8 + 3, 4094);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const uint32_t ka = k_base + prev_kvb * C::kTileBytes;
+        const uint32_t dsa = ds_base + b2 * C::kDSBytes;
+        // dQ = dS K   (M = 128 queries, N = d, K = 128 keys; A = dS MN-major, B = K MN-major)
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          sm100::mma_ss(tmem + C::kColDQ, sm100::sdesc_add(sm100::make_sdesc_sw128(dsa, kTile * 128, 1024), kk * 2048),
+                        sm100::sdesc_add(sm100::make_sdesc_sw128(ka, kTile * 128, 1024), kk * 2048), idesc_dq, kk > 0);
+        sm100::mma_commit(&ds_free[b2]);
+        sm100::mma_commit(dq_full);
+        if (prev_last) sm100::mma_commit(&kv_empty[prev_kvb]);   // K/V smem slot free
+      }
+      __syncwarp();
+    };
+    uint32_t t = 0;
+    while (cur.valid) {
+      TileIter nxt = cur;
+      nxt.advance(args.items);
+      const uint32_t st = t % C::kQStages, kvb = cur.item_c & 1;
+      const uint32_t st1 = (t + 1) % C::kQStages;
+#define MMA_TR(e) if (lane == 0 && t >= 40 && t < 48) sm100::trace_event(args.trace, 3328 + (t - 40) * 8 + (e), 4094)
+      MMA_TR(4);
+      // long wait (a compute phase): poll with back-off so the MMA warp does not steal issue slots
+#if !SIGATTN_DBG_MMAONLY
+      MMA_WAIT_P(&p_full[0], t & 1);
+#endif
+      if (lane == 0) sm100::trace_event(args.trace, 0 * 512 + t, 0 * 512 + 512);
+#if !SIGATTN_DBG_MMAONLY
+      if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);   // epilogue read previous dV/dK
+#endif
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
+      __syncwarp();
+      MMA_TR(0);
+      if (nxt.valid) {
+        if (nxt.i == 0) sm100::mbar_wait(&kv_full[nxt.item_c & 1], (nxt.item_c >> 1) & 1);
+        MMA_TR(5);
+        sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
+        MMA_TR(6);
+#if !SIGATTN_DBG_MMAONLY
+        if (kDQ) sm100::mbar_wait(&ds_copied[0], t & 1);   // dS^T(t, q0) left TMEM before S/dP(t+1, q0) land there
+#endif
+        MMA_TR(7);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          // the copy executes after every earlier MMA (tcgen05 ops of one thread run in order), so
+          // S/dP(i, q1) has finished reading the previous K/V columns
+          if (nxt.i == 0) copy_kv(nxt.item_c & 1);
+          mma1(nxt.item_c & 1, st1, 0);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
+#if !SIGATTN_DBG_MMAONLY
+      MMA_WAIT_P(&p_full[1], t & 1);
+#endif
+      if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        mma2(st, 1, false);
+        sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
+        if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
+        if (cur.i == 0 && args.counters) atomicAdd(args.counters + 1, (unsigned long long)cur.nqt);
+      }
+      __syncwarp();
+      MMA_TR(1);
+      if (nxt.valid) {
+#if !SIGATTN_DBG_MMAONLY
+        if (kDQ) sm100::mbar_wait(&ds_copied[1], t & 1);
+#endif
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 1);
+        __syncwarp();
+      }
+      MMA_TR(2);
+      prev_kvb = kvb;
+      prev_last = cur.i == cur.nqt - 1;
+      issue_dq(t);
+      if (lane == 0) sm100::trace_event(args.trace, 3 * 512 + t, 3 * 512 + 512);
+      cur = nxt;
+      ++t;
     }
   } else if (warp < kComputeWarps && !SIGATTN_DBG_MMAONLY) {
     // ===================== compute warps: all 16 work on each query half in turn =====================
-    // warpgroup w4 owns queries [16 w4, 16 w4 + 16) of each 64-query half (splitting the halves between
-    // two warp sets instead was measured 2-3% slower)
+    // warpgroup w4 owns queries [16 w4, 16 w4 + 16) of each 64-query half
     const uint32_t w4 = warp >> 2;
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
@@ -544,7 +567,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     // buffer instead put the reduce's smem read on the dS staging path: +2000 clk per tile.)
     constexpr uint32_t kEpiThread0 = 32 * kComputeWarps;
 #define EPI_TR(tt, e) if (threadIdx.x == kEpiThread0 && (tt) >= 40 && (tt) < 48) sm100::trace_event(args.trace, 3072 + ((tt) - 40) * 16 + (e), 4094)
-    auto drain_dq = [&](uint32_t tq, int zh, int i, int nq_) {
+    auto drain_dq = [&](uint32_t tq, int zh, int i) {
       sm100::mbar_wait(dq_full, tq & 1);
       EPI_TR(tq + 1, 7);
       sm100::tc_fence_after();
@@ -581,9 +604,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::fence_proxy_async_smem();
       sm100::named_bar_sync(1, 128);
       EPI_TR(tq + 1, 9);
-      if (args.peer_dq) {
-        peer_red_staged(args, buf, 2, kTile, D, zh, i * kTile, nq_, threadIdx.x - kEpiThread0);
-      } else if (threadIdx.x == kEpiThread0 && !SIGATTN_DBG_NORED) {
+      if (threadIdx.x == kEpiThread0 && !SIGATTN_DBG_NORED) {
         // rows past Nq are clipped by the TMA; padded query rows add exact zeros (dS = 0 there)
         sm100::tma_reduce_add_3d(&tmDQ, buf, 0, i * kTile, zh);
         sm100::tma_reduce_add_3d(&tmDQ, buf + kTile * 128, 32, i * kTile, zh);
@@ -593,7 +614,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     };
     uint32_t t = 0, item_c = 0;
     bool pend = false;            // a dQ tile waiting to be drained
-    int pend_zh = 0, pend_i = 0, pend_nq = 0;
+    int pend_zh = 0, pend_i = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
@@ -632,11 +653,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           }
           EPI_TR(t, qh == 0 ? 3 : 6);
         }
-        if (pend) drain_dq(t - 1, pend_zh, pend_i, pend_nq);
+        if (pend) drain_dq(t - 1, pend_zh, pend_i);
         pend = true;
         pend_zh = (int)zh;
         pend_i = i;
-        pend_nq = nq;
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
       sm100::mbar_wait_backoff(acc_full, item_c & 1);
@@ -682,8 +702,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       ++item_c;
     }
-    if (kDQ && pend) drain_dq(t - 1, pend_zh, pend_i, pend_nq);
-    if (kDQ && args.peer_dq) sm100::fence_sys();   // peer reductions before kernel completion
+    if (kDQ && pend) drain_dq(t - 1, pend_zh, pend_i);
     if (kDQ && threadIdx.x == kEpiThread0) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
   }
 

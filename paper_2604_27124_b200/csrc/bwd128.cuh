@@ -345,9 +345,7 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         }
         sm100::fence_proxy_async_smem();
         sm100::named_bar_sync(1, 128);
-        if (args.peer_dq) {
-          peer_red_staged(args, dqs, 4, C::kQT, D, (int)zh, i * C::kQT, nq, threadIdx.x - kEpiThread0);
-        } else if (threadIdx.x == kEpiThread0) {
+        if (threadIdx.x == kEpiThread0) {
 #pragma unroll
           for (int hh = 0; hh < 4; ++hh)
             sm100::tma_reduce_add_3d(&tmDQ, dqs + hh * (C::kQT * 128), hh * 32, i * C::kQT, (int)zh);
@@ -403,7 +401,6 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
   }
 
   if (kDQ && threadIdx.x == 32 * C::kWarpEpi) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
-  if (kDQ && args.peer_dq && warp >= C::kWarpEpi && warp < C::kWarpEpi + 4) sm100::fence_sys();   // peer reductions
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);

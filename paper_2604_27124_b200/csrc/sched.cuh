@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "sm100.cuh"
+
 #ifndef SIGATTN_DBG_NOFILL
 #define SIGATTN_DBG_NOFILL 0   // timing experiments only (outputs incomplete): skip the padded-row fills
 #endif
@@ -261,6 +263,27 @@ __global__ void cp_finalize_kernel(const float* __restrict__ acc, uint16_t* __re
   if (w0 < w1)
     dq_finalize_rows<kBf16>(acc + (size_t)zh * rows * D, out + (size_t)zh * rows * D, D, w0, w1, nloc,
                             threadIdx.x & 31, (size_t)D);
+}
+
+
+// Context-parallel push: this rank's complete fp32 partial acc [B, H, Nq, D] (summed over its key
+// tiles) -> reduce-added into the owners' accumulators peer[g] [B, H, rows, D] (g = row / rows),
+// valid rows only; each warp covers whole 256/512-byte rows (coalesced, one float4 per lane).  Ends
+// with a system-scope fence so the adds are performed before the kernel completes.
+__global__ void cp_push_kernel(const float* __restrict__ acc, float* const* __restrict__ peer, int rows, int H,
+                               int Nq, int D, const int32_t* __restrict__ lens) {
+  const int zh = blockIdx.y;
+  const int nq = clamp_len(lens, zh / H, Nq);
+  const int v4 = D / 4;   // float4 per row
+  const long long total = (long long)nq * v4;
+  const float4* src = reinterpret_cast<const float4*>(acc + (size_t)zh * Nq * D);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / v4), c = (int)(i % v4);
+    const int owner = r / rows, lr = r - owner * rows;
+    const float4 a = __ldcg(src + i);
+    sm100::red_add_v4_sys(peer[owner] + ((size_t)zh * rows + lr) * D + c * 4, a.x, a.y, a.z, a.w);
+  }
+  sm100::fence_sys();
 }
 
 // General (non-prefix) key_padding_mask [B, N] (1 = pad) -> a stable compaction per sequence:

@@ -273,7 +273,7 @@ template <int D, bool kBf16, bool kDQ = true, bool kDB = false>
 sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                           float* dq_acc, void* dk, void* dv,
                           const int4* items, const int* n_items, int max_items, cudaStream_t s,
-                          void* dq_pad = nullptr, const CpTarget* cp = nullptr) {
+                          void* dq_pad = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
   sigattn_status st;
@@ -283,7 +283,7 @@ sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* 
   if ((st = make_tmap(&tdo, dout, dt, 2, D, p->Nq, p->B, p->H, layout_bshd(p))) != SIGATTN_OK) return st;
   CUtensorMap tdq;   // fp32 dQ accumulator, 32-column boxes for the TMA reduce-add
   std::memset(&tdq, 0, sizeof(tdq));
-  if (kDQ && !cp && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, p->B, p->H, false)) != SIGATTN_OK)
+  if (kDQ && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, p->Nq, p->B, p->H, false)) != SIGATTN_OK)
     return st;
   BwdArgs a;
   a.items = items;
@@ -306,8 +306,6 @@ sigattn_status launch_bwd_t(const sigattn_params* p, const void* q, const void* 
   a.trace = g_trace;
   a.counters = g_counters;
   a.bshd = layout_bshd(p) ? 1 : 0;
-  a.peer_dq = cp ? cp->peer : nullptr;
-  a.peer_rows = cp ? cp->rows : 0;
   using C = BwdCfg<D>;
   auto kern = layout_bshd(p) ? sigattn_bwd_kernel<D, kBf16, kDQ, kDB, true> : sigattn_bwd_kernel<D, kBf16, kDQ, kDB, false>;
   if ((st = set_smem(kern, C::kSmemBytes)) != SIGATTN_OK) return st;
@@ -324,7 +322,7 @@ template <bool kBf16, bool kDQ = true, bool kDB = false>
 sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                              float* dq_acc, void* dk, void* dv,
                              const int4* items, const int* n_items, int max_items, cudaStream_t s,
-                             void* dq_pad = nullptr, const CpTarget* cp = nullptr) {
+                             void* dq_pad = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv, tdo;
   sigattn_status st;
@@ -334,7 +332,7 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   if ((st = make_tmap(&tdo, dout, dt, 2, 128, p->Nq, p->B, p->H, layout_bshd(p), Bwd128Cfg::kQT)) != SIGATTN_OK) return st;
   CUtensorMap tdq;   // fp32 dQ accumulator [B, H, Nq, 128], 32-column x 64-row boxes for the TMA reduce-add
   std::memset(&tdq, 0, sizeof(tdq));
-  if (kDQ && !cp && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 128, p->Nq, p->B, p->H, false,
+  if (kDQ && (st = make_tmap(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 128, p->Nq, p->B, p->H, false,
                                     Bwd128Cfg::kQT)) != SIGATTN_OK)
     return st;
   BwdArgs a;
@@ -358,8 +356,6 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
   a.trace = g_trace;
   a.counters = g_counters;
   a.bshd = layout_bshd(p) ? 1 : 0;
-  a.peer_dq = cp ? cp->peer : nullptr;
-  a.peer_rows = cp ? cp->rows : 0;
   auto kern = layout_bshd(p) ? sigattn_bwd128_kernel<kBf16, kDQ, kDB, true> : sigattn_bwd128_kernel<kBf16, kDQ, kDB, false>;
   if ((st = set_smem(kern, Bwd128Cfg::kSmemBytes)) != SIGATTN_OK) return st;
   const int grid = std::max(1, std::min(num_sms(), max_items));
@@ -375,16 +371,16 @@ sigattn_status launch_bwd128_t(const sigattn_params* p, const void* q, const voi
 template <int D, bool kBf16, bool kDQ = true>
 sigattn_status launch_bwd(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                           float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
-                          cudaStream_t s, void* dq_pad = nullptr, const CpTarget* cp = nullptr) {
-  return p->dbias ? launch_bwd_t<D, kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad, cp)
-                  : launch_bwd_t<D, kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad, cp);
+                          cudaStream_t s, void* dq_pad = nullptr) {
+  return p->dbias ? launch_bwd_t<D, kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad)
+                  : launch_bwd_t<D, kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad);
 }
 template <bool kBf16, bool kDQ = true>
 sigattn_status launch_bwd128(const sigattn_params* p, const void* q, const void* k, const void* v, const void* dout,
                              float* dq_acc, void* dk, void* dv, const int4* items, const int* n_items, int max_items,
-                             cudaStream_t s, void* dq_pad = nullptr, const CpTarget* cp = nullptr) {
-  return p->dbias ? launch_bwd128_t<kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad, cp)
-                  : launch_bwd128_t<kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad, cp);
+                             cudaStream_t s, void* dq_pad = nullptr) {
+  return p->dbias ? launch_bwd128_t<kBf16, kDQ, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad)
+                  : launch_bwd128_t<kBf16, kDQ, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s, dq_pad);
 }
 
 template <int D, bool kBf16, bool kF32>
@@ -701,7 +697,7 @@ extern "C" {
 
 size_t sigattn_bwd_cp_workspace_bytes(const sigattn_params* p) {
   if (check_params(p) != SIGATTN_OK) return 0;
-  return ws_items_bytes(p);
+  return ws_acc_bytes(p) + ws_items_bytes(p);
 }
 
 sigattn_status sigattn_fwd_cp(const sigattn_params* p, const sigattn_cp_params* cp, const void* q, const void* k,
@@ -743,24 +739,38 @@ sigattn_status sigattn_bwd_cp(const sigattn_params* p, const sigattn_cp_params* 
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dk) || !aligned16(dv) ||
       !aligned16(workspace))
     return fail(SIGATTN_EINVAL, "pointers must be 16-byte aligned");
-  if (workspace_bytes < ws_items_bytes(p))
-    return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(ws_items_bytes(p)) + " bytes");
+  const size_t need = ws_acc_bytes(p) + ws_items_bytes(p);
+  if (workspace_bytes < need)
+    return fail(SIGATTN_EWORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = sanitize_pad(p, q, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
   if ((st = sanitize_pad(p, dout, p->Nq, p->seqlens_q, s)) != SIGATTN_OK) return st;
   if ((st = sanitize_pad(p, k, p->Nk, p->seqlens_k, s)) != SIGATTN_OK) return st;
   if ((st = sanitize_pad(p, v, p->Nk, p->seqlens_k, s)) != SIGATTN_OK) return st;
-  const CpTarget t{cp->peer_acc, p->Nq / cp->world};
-  int* n_items = reinterpret_cast<int*>(workspace);
-  int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(workspace) + 16);
+  // dQ over this rank's keys accumulates in the local fp32 workspace (TMA reduce-adds in L2: every key
+  // tile adds a partial, so sending those over NVLink would multiply the traffic by the key-tile
+  // count), then one push kernel reduce-adds each valid row into its owner: the same bytes as a
+  // reduce-scatter, issued by our kernel over peer memory.
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  float* dq_acc = reinterpret_cast<float*>(ws);
+  int* n_items = reinterpret_cast<int*>(ws + ws_acc_bytes(p));
+  int4* items = reinterpret_cast<int4*>(ws + ws_acc_bytes(p) + 16);
   const int max_items = p->B * p->H * cdiv(p->Nk, 128);
-  if ((st = launch_bwd_prep(p, items, n_items, nullptr, s)) != SIGATTN_OK) return st;
+  if ((st = launch_bwd_prep(p, items, n_items, dq_acc, s)) != SIGATTN_OK) return st;
   const bool bf = p->dtype == SIGATTN_BF16;
   if (p->d == 64)
-    return bf ? launch_bwd<64, true>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s, nullptr, &t)
-              : launch_bwd<64, false>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s, nullptr, &t);
-  return bf ? launch_bwd128<true>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s, nullptr, &t)
-            : launch_bwd128<false>(p, q, k, v, dout, nullptr, dk, dv, items, n_items, max_items, s, nullptr, &t);
+    st = bf ? launch_bwd<64, true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s)
+            : launch_bwd<64, false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s);
+  else
+    st = bf ? launch_bwd128<true>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s)
+            : launch_bwd128<false>(p, q, k, v, dout, dq_acc, dk, dv, items, n_items, max_items, s);
+  if (st != SIGATTN_OK) return st;
+  const int rows = p->Nq / cp->world;
+  const dim3 grid(std::max(1, std::min(64, cdiv(p->Nq, 256))), p->B * p->H);
+  cp_push_kernel<<<grid, 256, 0, s>>>(dq_acc, cp->peer_acc, rows, p->H, p->Nq, p->d, p->seqlens_q);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return SIGATTN_OK;
 }
 
 sigattn_status sigattn_cp_finalize(const sigattn_params* p, int world, int rank, const float* acc, void* out,

@@ -17,11 +17,12 @@ Two ways to spread the work, both built on torch.distributed (NCCL on GPUs; gloo
                  dK_r, dV_r are complete (keys are owned); reduce-scatter(sum) dQ_r over query blocks.
 
    fused (fused=True): no partial tensor and no reduce-scatter.  Every rank maps
-   every rank's fp32 accumulator [B, H, N/G, d] (CUDA IPC, PeerAccumulators); the kernels'
-   epilogues reduce-add each partial O / dQ row straight into its owner's accumulator
-   (sigattn_fwd_cp / sigattn_bwd_cp, system-scope red.global.add over NVLink), overlapped with
-   the attention math tile by tile; a stream-ordered cross-rank barrier and sigattn_cp_finalize
-   (fp32 -> bf16, padded rows 0) complete the op.
+   every rank's fp32 accumulator [B, H, N/G, d] (CUDA IPC, PeerAccumulators).  The forward
+   kernel's epilogue reduce-adds each partial O row straight into its owner's accumulator
+   (sigattn_fwd_cp, system-scope red.global.add over NVLink), overlapped with the attention math of
+   the other tiles; the backward sums dQ over the rank's key tiles in L2 and a push kernel
+   reduce-adds each row into its owner (sigattn_bwd_cp).  A stream-ordered cross-rank barrier and
+   sigattn_cp_finalize (fp32 -> bf16, padded rows 0) complete the op.
 
 The attention calls default to the CUDA library (attention.sigattn_fwd / sigattn_bwd).  The `impl`
 hook exists so the CPU tests can drive the same orchestration through gloo with a stand-in; the
@@ -116,6 +117,8 @@ def _all_gather_into(buf: torch.Tensor, x: torch.Tensor, group=None) -> None:
 
 def _all_gather_seq(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """[B, H, n, d] blocks from every rank -> [B, H, world * n, d] in rank order."""
+    if world == 1:
+        return x.contiguous()
     B, H, n, d = x.shape
     buf = torch.empty((world * B, H, n, d), dtype=x.dtype, device=x.device)   # rank-major along dim 0
     _all_gather_into(buf, x.contiguous(), group=group)
@@ -124,6 +127,8 @@ def _all_gather_seq(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
 
 def _reduce_scatter_seq(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """[B, H, world * n, d] partial sums on every rank -> this rank's [B, H, n, d] block of the sum."""
+    if world == 1:
+        return x
     B, H, N, d = x.shape
     n = N // world
     src = x.reshape(B, H, world, n, d).permute(2, 0, 1, 3, 4).reshape(world * B, H, n, d).contiguous()

@@ -1,8 +1,10 @@
 #!/usr/bin/env python
 """Write the committed profile summary from a launch-list CSV and an ncu --set full report.
 
-usage: python scripts/profile_summary.py TAG   (reads gpurun_out/launches_TAG.csv, gpurun_out/prof_TAG.ncu-rep)
-writes profiles/TAG_launches.csv, profiles/TAG_ncu_raw.csv, profiles/TAG_summary.md, profiles/ncu_summary.json
+usage: python scripts/profile_summary.py TAG [WORKLOAD]   (reads gpurun_out/launches_TAG.csv,
+gpurun_out/prof_TAG.ncu-rep; WORKLOAD = the bench.py --workload the capture ran, default c3)
+writes profiles/TAG_launches.csv, profiles/TAG_ncu_raw.csv, profiles/TAG_summary.md and the WORKLOAD entry of
+profiles/ncu_summary.json (bench.py reads roofline.traffic from it)
 """
 import csv
 import io
@@ -32,7 +34,12 @@ def launch_shares(path):
     return per
 
 
-def main(tag):
+TITLES = {"c3": "C3 bench step: B=32 N=8192 H=12 d=64 jagged, bf16",
+          "c4": "C4 bench step: one 160M-encoder layer, B=16 N=8192 H=12 d=64, bf16",
+          "c5": "C5 bench step: N=16384 H=16 d=128 key-split CP, bf16"}
+
+
+def main(tag, workload="c3"):
     out = os.path.join(ROOT, "profiles")
     lpath = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     rep = os.path.join(ROOT, "gpurun_out", f"prof_{tag}.ncu-rep")
@@ -66,7 +73,7 @@ def main(tag):
         kern[name] = d
     per = launch_shares(lpath)
     tot = sum(sum(v) for v in per.values())
-    lines = [f"# Profile summary `{tag}` (C3 bench step: B=32 N=8192 H=12 d=64 jagged, bf16)", "",
+    lines = [f"# Profile summary `{tag}` ({TITLES.get(workload, workload)})", "",
              "Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`, cold-cache, serialised;",
              "compare shares, not absolutes):", "", "| kernel | launches | mean us | share of step |", "|---|---|---|---|"]
     for k, v in per.items():
@@ -77,16 +84,21 @@ def main(tag):
         lines.append(f"| {k} | " + " | ".join(
             (f"{kern[n].get(k):.4g}" if isinstance(kern[n].get(k), float) else str(kern[n].get(k))) for n in kern) + " |")
     open(os.path.join(out, f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
-    bwd = next((v for n, v in kern.items() if "bwd_kernel" in n), {})
-    fwd = next((v for n, v in kern.items() if "fwd_kernel" in n), {})
-    summ = {"tag": tag,
+    bwd = next((v for n, v in kern.items() if "bwd_kernel" in n or "bwd128_kernel" in n), {})
+    fwd = next((v for n, v in kern.items() if "fwd_kernel" in n or "fwd2_kernel" in n), {})
+    entry = {"tag": tag,
             "bwd_kernel": {"dram_bytes_per_launch": bwd.get("dram__bytes_read.sum", 0) + bwd.get("dram__bytes_write.sum", 0),
                            "duration_ms": bwd.get("gpu__time_duration.sum")},
             "fwd_kernel": {"dram_bytes_per_launch": fwd.get("dram__bytes_read.sum", 0) + fwd.get("dram__bytes_write.sum", 0),
                            "duration_ms": fwd.get("gpu__time_duration.sum")}}
-    json.dump(summ, open(os.path.join(out, "ncu_summary.json"), "w"), indent=1)
+    jp = os.path.join(out, "ncu_summary.json")
+    summ = json.load(open(jp)) if os.path.exists(jp) else {}
+    if "tag" in summ:   # round-1 flat format: the C3 capture
+        summ = {"c3": summ}
+    summ[workload] = entry
+    json.dump(summ, open(jp, "w"), indent=1)
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "c3")
