@@ -52,8 +52,12 @@ def build_trace() -> str:
 
 
 def build_variant(name: str, defines) -> str:
-    """Experimental build with extra -D flags -> libsigattn_<name>.so (selected with $SIGATTN_LIB)."""
+    """Experimental build with extra -D flags -> libsigattn_<name>.so (selected with $SIGATTN_LIB).
+    Timing-only SIGATTN_DBG_* switches (wrong results, csrc/debug.cuh) get -DSIGATTN_DEBUG_BUILD."""
     out = os.path.join(PKG, f"libsigattn_{name}.so")
+    defines = list(defines)
+    if any(d.startswith("SIGATTN_DBG_") for d in defines):
+        defines.append("SIGATTN_DEBUG_BUILD")
     cmd = [NVCC] + NVCC_FLAGS + [f"-D{d}" for d in defines] + [os.path.join(CSRC, "sigattn.cu"), "-o", out]
     subprocess.check_call(cmd)
     return out

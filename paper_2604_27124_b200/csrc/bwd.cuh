@@ -22,9 +22,11 @@
 // which the warp scheduler favours):
 //   warps 0-15  compute: thread = key row (TMEM lane); all 16 warps process query half 0, then half 1;
 //               warpgroup w takes 16 queries [64q + 16w, +16) of half q
-//   warps 16-19 epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> red.global.add.v4.f32),
-//               dK/dV of a finished key tile (x alpha for dK, round, store; padded rows = 0)
-//   warp 20     TMA: K_j, V_j (2 slots), Q_i + dO_i (3 stages)
+//   warps 16-19 epilogue warpgroup: dS^T staging (TMEM -> swizzled smem operand of the dQ MMA), dQ_i
+//               drain (tcgen05.ld -> x alpha -> swizzled fp32 smem tile -> two TMA bulk tensor
+//               reduce-adds into the fp32 workspace, in L2), dK/dV of a finished key tile (x alpha
+//               for dK, round, store; padded rows = 0)
+//   warp 20     TMA: K_j, V_j (2 slots), Q_i + dO_i (2 stages)
 //   warp 21     MMA issuer (one elected thread); also tcgen05.cp of K_j, V_j into TMEM
 //   warp 22     TMEM allocator
 // TMEM (d = 64): S^T [0,128) dP^T [128,256) dV [256,320) dK [320,384) dQ [384,448) K [448,480) V [480,512)
@@ -43,32 +45,11 @@
 #else
 #define MMA_WAIT_P(b, p) sm100::mbar_wait_backoff(b, p)
 #endif
-#ifndef SIGATTN_DBG_NOCOMPUTE
-#define SIGATTN_DBG_NOCOMPUTE 0   // timing experiments only (wrong results): compute warps skip sigma + TMEM I/O
-#endif
-#ifndef SIGATTN_DBG_EPI_NOLD
-#define SIGATTN_DBG_EPI_NOLD 0    // timing experiments only: epilogue skips TMEM loads and global writes
-#endif
-#ifndef SIGATTN_DBG_NORED
-#define SIGATTN_DBG_NORED 0       // timing experiments only: skip the dQ reduce-add into global memory
-#endif
-#ifndef SIGATTN_DBG_NOSTAGE
-#define SIGATTN_DBG_NOSTAGE 0     // timing experiments only (wrong results): epilogue skips the dS smem staging
-#endif
 #ifndef SIGATTN_BWD_SPEC
 #define SIGATTN_BWD_SPEC 1        // tier-4 sigma evaluated before the warp vote (sigma_row_spec4)
 #endif
 #ifndef SIGATTN_BWD64_SPEC
 #define SIGATTN_BWD64_SPEC false  // ... in the d = 64 fused backward: vote first measured 1.5-8% faster
-#endif
-#ifndef SIGATTN_BWD_EMU
-#define SIGATTN_BWD_EMU 0         // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
-#endif
-#ifndef SIGATTN_DBG_NOTMA_QDO
-#define SIGATTN_DBG_NOTMA_QDO 0   // timing experiments only: Q/dO tiles loaded once, then reused (stale)
-#endif
-#ifndef SIGATTN_DBG_MMAONLY
-#define SIGATTN_DBG_MMAONLY 0     // timing experiments only: MMA + TMA pipeline alone (no compute/epilogue waits)
 #endif
 namespace sigattn {
 
@@ -160,7 +141,7 @@ __device__ __forceinline__ void bwd_sigma16(float (&v)[16], float a2, float b2, 
   if constexpr (!kSpec) {   // vote first (measured better for the d = 64 fused backward)
     (void)s_taddr;
     (void)spec;
-    sigma_row<16, kMask, SIGATTN_BWD_EMU>(v, a2, b2, key_valid, nvalid);
+    sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid);
     return;
   }
 #if SIGATTN_BWD_SPEC
@@ -176,7 +157,7 @@ __device__ __forceinline__ void bwd_sigma16(float (&v)[16], float a2, float b2, 
 #else
   (void)s_taddr;
   (void)spec;
-  sigma_row<16, kMask, SIGATTN_BWD_EMU>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
+  sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
 #endif
 }
 

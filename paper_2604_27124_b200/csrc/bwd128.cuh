@@ -9,7 +9,8 @@
 //     dV_j += P^T dO_i,   dK_j += dS^T Q_i           TS (P^T, dS^T in TMEM), N = d = 128
 //     dQ_i^T = K_j^T dS_i^T                          SS, M = d, N = 64 queries, K = keys
 //                                                    (A = K read MN-major, B = dS^T smem MN-major)
-// dQ^T is drained lane = d index and reduce-added (coalesced over d) into the fp32 workspace; alpha
+// dQ^T is drained lane = d index into a swizzled fp32 smem tile [64 q][128 d] (four SW128 boxes of
+// 32 columns) and added into the fp32 workspace by four TMA bulk tensor reduce-adds (in L2); alpha
 // is applied in the epilogues.  MMA order per tile: dV/dK(i) | S,dP(i+1) | dQ(i), so
 // the compute warps start on tile i+1 while dQ(i) runs.
 // Roles as in bwd.cuh (768 threads): warps 0-15 compute (warpgroup w: queries [16w, 16w+16) of the

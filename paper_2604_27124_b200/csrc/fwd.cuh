@@ -24,17 +24,8 @@
 #include "sigmoid.cuh"
 #include "sm100.cuh"
 
-#ifndef SIGATTN_DBG_FWD_NOSIGMA
-#define SIGATTN_DBG_FWD_NOSIGMA 0
-#endif
-#ifndef SIGATTN_DBG_FWD_NOTMA_KV
-#define SIGATTN_DBG_FWD_NOTMA_KV 0   // timing experiments only (wrong results): K/V tiles loaded once per slot, then reused
-#endif
 #ifndef SIGATTN_FWD_SPEC
 #define SIGATTN_FWD_SPEC 1  // tier-4 sigma evaluated before the warp vote (sigma_row_spec4)
-#endif
-#ifndef SIGATTN_FWD_EMU
-#define SIGATTN_FWD_EMU 0   // every k-th element pair takes the FMA-pipe exp2 (0: all on MUFU)
 #endif
 
 namespace sigattn {
@@ -112,7 +103,7 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 template <bool kMask, bool kBf16>
 __device__ __forceinline__ void sigmoid_row32(float (&v)[32], uint32_t (&pk)[16], float a, float c, bool row_valid,
                                               int nvalid) {
-  sigma_row<32, kMask, SIGATTN_FWD_EMU>(v, a, c, row_valid, nvalid);
+  sigma_row<32, kMask, 0>(v, a, c, row_valid, nvalid);
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
     float p0 = v[e], p1 = v[e + 1];

@@ -7,11 +7,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "debug.cuh"
 #include "sm100.cuh"
 
-#ifndef SIGATTN_DBG_NOFILL
-#define SIGATTN_DBG_NOFILL 0   // timing experiments only (outputs incomplete): skip the padded-row fills
-#endif
 
 namespace sigattn {
 
