@@ -46,7 +46,8 @@ __device__ __forceinline__ void sigma_pair_t(float t0, float t1, float& p0, floa
     }
     float r0, r1;
     if constexpr (kTier == 4) {
-      ffma2(r0, r1, u0, u1, kL1, kL1, kL0, kL0);      // L0 + L1 u
+      r0 = 1.0f - u0;                                 // u (1 - u)
+      r1 = 1.0f - u1;
     } else {
       ffma2(r0, r1, u0, u1, kR2, kR2, kR1, kR1);
       ffma2(r0, r1, r0, r1, u0, u1, kR0, kR0);        // R(u)
@@ -243,23 +244,85 @@ void run_pipe(const char* name, int threads, long long* cyc, uint32_t* sink, flo
   printf("  %-44s warps %2d  %6.2f elem/clk/SM\n", name, threads / 32, (double)threads * 32 * iters / c);
 }
 
+
+// production forward chunk path (fwd.cuh sigmoid_chunk32 logic: spec tier 4, reload on vote failure)
+// at chunk width kW (16 or 32 columns per load), any warp count up to 32
+template <int kW>
+__global__ void __launch_bounds__(1024, 1) kern_w(int iters, long long* cyc, uint32_t* sink, float bias2) {
+  __shared__ uint32_t tmem_holder;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0) sm100::tmem_alloc<512>(&tmem_holder);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_holder;
+  const uint32_t lane_addr = ((warp & 3) * 32) << 16;
+  const uint32_t col = (warp >> 2) * 64;
+  {
+    uint32_t v[16];
+    for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(((lane * 7 + i * 13) % 31 - 15) * 0.5f);
+    sm100::tmem_st16(tmem + lane_addr + col, v);
+    sm100::tmem_st16(tmem + lane_addr + col + 16, v);
+    sm100::tmem_wait_st();
+  }
+  __syncthreads();
+  bool spec = true;
+  uint32_t acc = 0;
+  const float a2 = 0.125f * 1.4426950408889634f;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float r[kW];
+    uint32_t pk[kW / 2];
+    if constexpr (kW == 32) sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+    else {
+      sm100::tmem_ld16(tmem + lane_addr + col, r);
+      sm100::tmem_wait_ld_dep16(r);
+    }
+    bool done = false;
+    if (spec) {
+      done = sigma_row_spec4<kW, false>(r, a2, bias2, true, kW);
+      if (!done) {
+        if constexpr (kW == 32) sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+        else { sm100::tmem_ld16(tmem + lane_addr + col, r); sm100::tmem_wait_ld_dep16(r); }
+      }
+    }
+    if (!done) spec = sigma_row<kW, false, 0>(r, a2, bias2, true, kW) == 4;
+#pragma unroll
+    for (int e = 0; e < kW; e += 2) pk[e >> 1] = sm100::pack2<true>(r[e], r[e + 1]);
+    if constexpr (kW == 32) sm100::tmem_st16(tmem + lane_addr + col + 32, pk);
+    else sm100::tmem_st8(tmem + lane_addr + col + 32, pk);
+    if ((it & 3) == 3) sm100::tmem_wait_st();
+#pragma unroll
+    for (int i = 0; i < kW / 2; ++i) acc ^= pk[i];
+  }
+  long long t1 = clock64();
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc<512>(tmem);
+}
+template <int kW>
+void run_w(int warps, long long* cyc, uint32_t* sink, float bias2) {
+  const int iters = 4000;
+  kern_w<kW><<<148, warps * 32>>>(iters, cyc, sink, bias2);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return; }
+  long long c;
+  cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("  production chunk path, %2d columns per load, warps %2d  %6.2f elem/clk/SM\n", kW, warps,
+         (double)warps * 32 * kW * iters / c);
+}
+
 int main() {
   long long* cyc;
   uint32_t* sink;
   cudaMalloc(&cyc, 148 * 8);
   cudaMalloc(&sink, 148 * 512 * 4);
   const float b4 = -13.0f, b0 = 0.0f;   // t = s a2 + b2: tier 4 (b = -log 8192 -> b2 ~ -13) / exact tier
-  for (int threads : {512}) {
-    run<0, true, 1>("tier4 spec, MUFU only", threads, cyc, sink, b4);
-    run<0, true, 1, 1>("tier4 spec, registers only (no TMEM)", threads, cyc, sink, b4);
-    run<1, true, 1, 1>("all-FMA exp2, registers only", threads, cyc, sink, b4);
-    run<1, true, 1, 3>("all-FMA exp2, ld only", threads, cyc, sink, b4);
-    run<1, true, 1, 0>("all-FMA exp2, ld+st", threads, cyc, sink, b4);
-    run<2, true, 1, 1>("half-FMA exp2, registers only", threads, cyc, sink, b4);
-    run<2, true, 1, 0>("half-FMA exp2, ld+st", threads, cyc, sink, b4);
-    run<0, true, 1, 3>("tier4 spec, ld only", threads, cyc, sink, b4);
-    run<0, true, 1, 5>("tier4 spec, ld x16 x2", threads, cyc, sink, b4);
-    run<0, true, 1, 6>("tier4 spec, ld 16x256b.x8", threads, cyc, sink, b4);
+  for (int w : {8, 16, 24, 32}) {
+    run_w<32>(w, cyc, sink, b4);
+    run_w<16>(w, cyc, sink, b4);
   }
   return 0;
 }
