@@ -52,6 +52,9 @@ struct FwdArgs {
   // partial O row of query q is reduce-added into peer_o[q / peer_rows] at row q % peer_rows
   float* const* peer_o;
   int peer_rows;
+  // two-tile forward (fwd2.cuh) with a tail split (split_tail_block): fp32 piece buffer
+  // [pieces][2 tiles][128][D], or nullptr when the work list has no split items
+  float* split_acc;
 };
 
 // fp32 partial O row -> the owning rank's accumulator (context parallelism, A4: P:121).  32 values

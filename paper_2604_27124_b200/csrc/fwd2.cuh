@@ -107,6 +107,12 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     const int nq = clampi(args.seqlens_q ? args.seqlens_q[b] : args.Nq, 0, args.Nq);
     return 2 * pi + 1 < (nq + kTile - 1) / kTile;
   };
+  // work item (b, h, query-tile pair) over key tiles [kb, kb + nkt); piece >= 0: one key-range piece
+  // of a split tail item (split_tail_block), whose fp32 partial O goes to the piece buffer
+  struct Item2 {
+    int b, h, pi, kb, nkt, piece;
+  };
+  auto decode = [](int4 it) { return Item2{it.x & 0xFFFF, it.y, it.z & 0xFFFF, it.z >> 16, it.w, (it.x >> 16) - 1}; };
 
   if (warp == C::kWarpTMA) {
     // ===================== TMA producer =====================
@@ -114,8 +120,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     const uint64_t pol_kv = sm100::policy_evict_last();
     uint32_t kv_it = 0, c = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
-      const int4 item = args.items[it];
-      const int b = item.x, h = item.y, pi = item.z, nkt = item.w;
+      const Item2 item = decode(args.items[it]);
+      const int b = item.b, h = item.h, pi = item.pi, nkt = item.nkt, kb = item.kb;
       if (nkt <= 0) continue;
       const int zh = b * args.H + h;
       const int ntq = has_b(b, pi) ? 2 : 1;
@@ -141,7 +147,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 #pragma unroll
             for (int s = 0; s < C::kSub; ++s)
               sm100::tma_load_bh(smem + C::kKOff + st * C::kTileBytes + s * (kTile * 128), &tmK, &k_full[st], s * 64,
-                                 j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+                                 (kb + j) * kTile, zh, pol_kv, args.bshd ? args.H : 0);
           }
         }
         __syncwarp();
@@ -154,7 +160,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 #pragma unroll
             for (int s = 0; s < C::kSub; ++s)
               sm100::tma_load_bh(smem + C::kVOff + st * C::kTileBytes + s * (kTile * 128), &tmV, &v_full[st], s * 64,
-                                 j * kTile, zh, pol_kv, args.bshd ? args.H : 0);
+                                 (kb + j) * kTile, zh, pol_kv, args.bshd ? args.H : 0);
           }
         }
         __syncwarp();
@@ -172,10 +178,10 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     uint32_t xs[2] = {0, 0};   // S / P phase counter per query-tile slot
     uint32_t xo[2] = {0, 0};   // O phase counter per slot
     for (int it = first_item(); it < n_items; it = next_item(it)) {
-      const int4 item = args.items[it];
-      const int nkt = item.w;
+      const Item2 item = decode(args.items[it]);
+      const int nkt = item.nkt;
       if (nkt <= 0) continue;
-      const int ntq = has_b(item.x, item.z) ? 2 : 1;
+      const int ntq = has_b(item.b, item.pi) ? 2 : 1;
       if (args.counters && sm100::elect_one()) atomicAdd(args.counters, (unsigned long long)(ntq * nkt));
       __syncwarp();
       const uint32_t qb = c % C::kQBufs;
@@ -222,26 +228,36 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         __syncwarp();
         ++xs[x];
       };
+      // the Q pair is released once the item's LAST S MMAs complete (PV does not read Q), so the next
+      // item's Q loads during the last key tiles' sigma and PV instead of after them
+      auto release_q = [&]() {
+        if (sm100::elect_one()) sm100::mma_commit(&q_empty[qb]);
+        __syncwarp();
+      };
       for (int x = 0; x < ntq; ++x) issue_s(x, 0);
+      if (nkt == 1) release_q();
       if constexpr (C::kSepP) {
         // events arrive as s_free_A(j), s_free_B(j), p_full_A(j), p_full_B(j): issue in that order
         for (int j = 0; j < nkt; ++j) {
-          if (j + 1 < nkt)
+          if (j + 1 < nkt) {
             for (int x = 0; x < ntq; ++x) {
               sm100::mbar_wait(&s_free[x], xs[x] & 1);   // pair x has read S_x(j)
               issue_s(x, j + 1);
             }
+            if (j + 2 == nkt) release_q();
+          }
           for (int x = 0; x < ntq; ++x) issue_pv(x, j);
         }
       } else {
-        for (int j = 0; j < nkt; ++j)
+        for (int j = 0; j < nkt; ++j) {
           for (int x = 0; x < ntq; ++x) {
             issue_pv(x, j);                      // reads P_x(j) out of the S_x buffer ...
             if (j + 1 < nkt) issue_s(x, j + 1);  // ... which S_x(j+1) then overwrites (in-order)
           }
+          if (j + 2 == nkt) release_q();
+        }
       }
       if (sm100::elect_one()) {
-        sm100::mma_commit(&q_empty[qb]);
         for (int x = 0; x < ntq; ++x) sm100::mma_commit(&o_full[x]);
       }
       __syncwarp();
@@ -259,8 +275,8 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     bool spec = true;   // speculate tier 4 while the last chunk took it
     uint32_t xs = 0, xo = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
-      const int4 item = args.items[it];
-      const int b = item.x, h = item.y, pi = item.z, nkt = item.w;
+      const Item2 item = decode(args.items[it]);
+      const int b = item.b, h = item.h, pi = item.pi, nkt = item.nkt, kb = item.kb;
       if (nkt <= 0) continue;
       if (x == 1 && !has_b(b, pi)) continue;     // odd tile count: no second tile in this item
       const int qt = 2 * pi + (int)x;
@@ -276,7 +292,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           const uint32_t col = x * 128 + gp * 64 + ch * 32;
-          const int nvalid = nk - (j * kTile + (int)gp * 64 + ch * 32);
+          const int nvalid = nk - ((kb + j) * kTile + (int)gp * 64 + ch * 32);
           float r[32];
           uint32_t pk[16];
           sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
@@ -328,6 +344,13 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         }
         if (kOutF32 && args.peer_o) {
           if (valid) peer_red_row32(args, D, b, h, qrow, c0, ov);
+        } else if (item.piece >= 0) {   // a piece of a split tail item: fp32 partial into its slot
+          float4* dst = reinterpret_cast<float4*>(args.split_acc + ((size_t)(item.piece * 2 + x) * kTile + row) * D + c0);
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            dst[e >> 2] = valid ? make_float4(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1]),
+                                              __uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3]))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
         } else if (qrow < args.Nq) {
           if constexpr (kOutF32) {
             float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + rowoff + c0);

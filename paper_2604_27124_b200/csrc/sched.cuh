@@ -15,6 +15,8 @@ namespace sigattn {
 
 constexpr int kSchedThreads = 1024;
 constexpr int kMaxSchedB = 4096;      // sequences per batch the single-block builder supports
+constexpr int kMaxTail = 128;         // tail items the kind-2 split handles (m <= G / 2, G <= 256 CTAs)
+constexpr int kMinPiece = 8;          // key tiles per piece of a split tail item (at least)
 
 // Work items of this CTA in a persistent grid: rounds of gridDim.x consecutive items of the
 // longest-first list, dealt boustrophedon (even rounds by CTA index, odd rounds reversed), so the
@@ -90,12 +92,55 @@ __device__ __forceinline__ void build_worklist_block(int kind, int B, int H, int
   }
 }
 
+// Tail split of a kind-2 list for a persistent grid of G CTAs (the d = 128 forward).  Items are
+// dealt in rounds of G; with R full rounds and m < G/2 items left, the last round would keep only m
+// CTAs busy (equal-cost items -- e.g. a uniformly padded batch -- leave up to a whole item of tail).
+// Each of the m tail items is cut along its KEY range into up to G/m pieces, so the last round fills
+// the grid with short pieces.  Sigmoid attention is additive over key blocks, so a piece
+// writes its partial O (fp32, both query tiles) into its own slot of a piece buffer and
+// fwd_split_finalize_kernel sums the pieces of each split item: plain stores, no atomics, no zeroing,
+// deterministic.  Encoding of a piece: x = b | (piece + 1) << 16, z = pair | first key tile << 16,
+// w = key tiles of the piece; map[slot] = (b, h, pair, first piece | pieces << 16).
+__device__ __forceinline__ void split_tail_block(int G, int4* __restrict__ items, int* __restrict__ n_items,
+                                                 int4* __restrict__ map, int* __restrict__ n_split) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int n = *n_items, R = n / G, m = n - R * G;
+  int nsplit = 0;
+  if (R >= 1 && m > 0 && 2 * m <= G) {
+    const int s = G / m;
+    int4 tail[kMaxTail];
+    for (int t = 0; t < m; ++t) tail[t] = items[R * G + t];
+    int pos = R * G, piece = 0;
+    for (int t = 0; t < m; ++t) {
+      const int4 it = tail[t];
+      // pieces of at least kMinPiece key tiles: a piece pays a Q load, a pipeline fill and drain and an
+      // fp32 round trip, which short items do not recover (measured: d = 128, 12-tile items -4%)
+      const int nkt = it.w, si = max(1, min(s, nkt / kMinPiece)), c = (nkt + si - 1) / si, p = (nkt + c - 1) / c;
+      if (p <= 1) {
+        items[pos++] = it;
+        continue;
+      }
+      map[nsplit++] = make_int4(it.x, it.y, it.z, piece | (p << 16));
+      for (int q = 0; q < p; ++q, ++piece) {
+        const int kb = q * c;
+        items[pos++] = make_int4(it.x | ((piece + 1) << 16), it.y, it.z | (kb << 16), min(c, nkt - kb));
+      }
+    }
+    *n_items = pos;
+  }
+  *n_split = nsplit;
+}
+
 __global__ void __launch_bounds__(kSchedThreads)
 build_worklist_kernel(int kind, int B, int H, int Nq, int Nk, const int32_t* __restrict__ seqlens_q,
-                      const int32_t* __restrict__ seqlens_k, int4* __restrict__ items, int* __restrict__ n_items) {
+                      const int32_t* __restrict__ seqlens_k, int4* __restrict__ items, int* __restrict__ n_items,
+                      int split_grid, int4* __restrict__ split_map, int* __restrict__ n_split) {
   extern __shared__ int sh[];
   build_worklist_block(kind, B, H, Nq, Nk, seqlens_q, seqlens_k, items, n_items, sh);
+  if (kind == 2 && split_grid > 0) split_tail_block(split_grid, items, n_items, split_map, n_split);
 }
+
 
 // Backward prologue, one launch: CTA 0 builds the backward work list while CTAs 1.. zero the fp32
 // dQ accumulator on valid query rows [0, n_q[b]).  Padded accumulator rows are never read (the
@@ -376,6 +421,39 @@ __global__ void mask_to_seqlens_kernel(const uint8_t* __restrict__ mask, int N, 
     for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) { v += s_valid[i]; f = min(f, s_first[i]); }
     seqlens[b] = v;
     if (v != f) atomicExch(nonprefix, 1);
+  }
+}
+
+// Sum of the pieces of every split item (split_tail_block) -> the 16-bit O rows of its two query
+// tiles (rows >= n_q exact 0).  One CTA per split slot; acc: [pieces][2 tiles][128][D] fp32.
+template <bool kBf16>
+__global__ void fwd_split_finalize_kernel(const float* __restrict__ acc, const int4* __restrict__ map,
+                                          const int* __restrict__ n_split, uint16_t* __restrict__ out, int H, int Nq,
+                                          int D, const int32_t* __restrict__ lens, int bshd) {
+  const int slot = blockIdx.x;
+  if (slot >= *n_split) return;
+  const int4 mp = map[slot];
+  const int b = mp.x & 0xFFFF, h = mp.y, pi = mp.z & 0xFFFF, first = mp.w & 0xFFFF, np = mp.w >> 16;
+  const int nq = clamp_len(lens, b, Nq);
+  const int v8 = D / 8;
+  for (int i = threadIdx.x; i < 2 * 128 * v8; i += blockDim.x) {
+    const int x = i / (128 * v8), r = (i / v8) % 128, c = (i % v8) * 8;
+    const int qrow = (2 * pi + x) * 128 + r;
+    if (qrow >= Nq) continue;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (qrow < nq)
+      for (int p = 0; p < np; ++p) {
+        const float4* src = reinterpret_cast<const float4*>(acc + ((size_t)((first + p) * 2 + x) * 128 + r) * D + c);
+        const float4 u = __ldcg(src), w = __ldcg(src + 1);
+        a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w;
+        a[4] += w.x; a[5] += w.y; a[6] += w.z; a[7] += w.w;
+      }
+    uint4 o;
+    o.x = sm100::pack2<kBf16>(a[0], a[1]);
+    o.y = sm100::pack2<kBf16>(a[2], a[3]);
+    o.z = sm100::pack2<kBf16>(a[4], a[5]);
+    o.w = sm100::pack2<kBf16>(a[6], a[7]);
+    *reinterpret_cast<uint4*>(out + row_off(bshd, H, Nq, D, b, h, qrow) + c) = o;
   }
 }
 

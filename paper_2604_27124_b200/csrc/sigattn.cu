@@ -192,14 +192,16 @@ sigattn_status set_smem(K kernel, int bytes) {
 
 int sched_smem(const sigattn_params* p) { return (4 * p->B + 1) * (int)sizeof(int); }
 
-sigattn_status launch_worklist(int kind, const sigattn_params* p, int4* items, int* n_items, cudaStream_t s) {
+// split_grid > 0 (kind 2): cut the last round's items along their key range (split_tail_block)
+sigattn_status launch_worklist(int kind, const sigattn_params* p, int4* items, int* n_items, cudaStream_t s,
+                               int split_grid = 0, int4* split_map = nullptr, int* n_split = nullptr) {
   const int smem = sched_smem(p);
   if (smem > 48 * 1024) {
     sigattn_status st = set_smem(build_worklist_kernel, (4 * kMaxSchedB + 1) * (int)sizeof(int));
     if (st != SIGATTN_OK) return st;
   }
   build_worklist_kernel<<<1, kSchedThreads, smem, s>>>(kind, p->B, p->H, p->Nq, p->Nk, p->seqlens_q, p->seqlens_k,
-                                                        items, n_items);
+                                                        items, n_items, split_grid, split_map, n_split);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return SIGATTN_OK;
@@ -223,7 +225,7 @@ sigattn_status launch_bwd_prep(const sigattn_params* p, int4* items, int* n_item
 template <int D, bool kBf16, bool kF32>
 sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k, const void* v, void* o,
                           const int4* items, const int* n_items, int max_items, cudaStream_t s,
-                          const CpTarget* cp = nullptr) {
+                          const CpTarget* cp = nullptr, float* split_acc = nullptr) {
   const CUtensorMapDataType dt = kBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv;
   sigattn_status st;
@@ -249,6 +251,7 @@ sigattn_status launch_fwd(const sigattn_params* p, const void* q, const void* k,
   a.bshd = layout_bshd(p) ? 1 : 0;
   a.peer_o = cp ? cp->peer : nullptr;
   a.peer_rows = cp ? cp->rows : 0;
+  a.split_acc = split_acc;
   const int grid = std::max(1, std::min(num_sms(), max_items));
   if constexpr (use_fwd2(D)) {
     using C = Fwd2Cfg<D>;
@@ -437,8 +440,16 @@ size_t ws_items_bytes(const sigattn_params* p) {
 size_t ws_items_q_bytes(const sigattn_params* p) {   // query-tile work list (deterministic dQ pass)
   return align_up(16 + (size_t)p->B * p->H * cdiv(p->Nq, 128) * sizeof(int4), 256);
 }
-size_t ws_fwd_bytes(const sigattn_params* p) {   // forward work list: {count, pad} + items
-  return align_up(16 + (size_t)p->B * p->H * cdiv(p->Nq, 128) * sizeof(int4), 256);
+// Forward workspace: {count, split count, pad} + items (+ grid spare entries for the pieces of a
+// tail split), then, for the two-tile forward, the split map [grid] and the fp32 piece buffer
+// [grid][2][128][d] (split_tail_block).
+int fwd_split_grid(const sigattn_params* p) { return use_fwd2(p->d) ? num_sms() : 0; }
+size_t ws_fwd_items_bytes(const sigattn_params* p) {
+  return align_up(16 + ((size_t)p->B * p->H * cdiv(p->Nq, 128) + fwd_split_grid(p)) * sizeof(int4), 256);
+}
+size_t ws_fwd_bytes(const sigattn_params* p) {
+  const size_t G = (size_t)fwd_split_grid(p);
+  return ws_fwd_items_bytes(p) + align_up(G * sizeof(int4), 256) + G * 2 * 128 * p->d * sizeof(float);
 }
 
 }  // namespace
@@ -526,9 +537,16 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
   }
   const bool f32 = (p->flags & SIGATTN_F_OUT_F32_PARTIAL) != 0;
   const int max_items = p->B * p->H * cdiv(p->Nq, 128);
-  int* n_items = reinterpret_cast<int*>(workspace);
-  int4* items = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(workspace) + 16);
-  st = launch_worklist(fwd_item_kind(p->d), p, items, n_items, s);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  int* n_items = reinterpret_cast<int*>(ws);
+  int* n_split = n_items + 1;
+  int4* items = reinterpret_cast<int4*>(ws + 16);
+  // tail split: the two-tile forward with 16-bit output (fp32 partials keep whole items)
+  const int G = f32 ? 0 : fwd_split_grid(p);
+  int4* split_map = reinterpret_cast<int4*>(ws + ws_fwd_items_bytes(p));
+  float* split_acc = G ? reinterpret_cast<float*>(ws + ws_fwd_items_bytes(p) + align_up((size_t)G * sizeof(int4), 256))
+                       : nullptr;
+  st = launch_worklist(fwd_item_kind(p->d), p, items, n_items, s, G, split_map, n_split);
   if (st == SIGATTN_OK) {
     const bool bf = p->dtype == SIGATTN_BF16;
     if (p->d == 64) {
@@ -538,10 +556,20 @@ sigattn_status sigattn_fwd(const sigattn_params* p, const void* q, const void* k
                     : launch_fwd<64, false, false>(p, q, k, v, o, items, n_items, max_items, s);
     } else {
       if (bf) st = f32 ? launch_fwd<128, true, true>(p, q, k, v, o, items, n_items, max_items, s)
-                       : launch_fwd<128, true, false>(p, q, k, v, o, items, n_items, max_items, s);
+                       : launch_fwd<128, true, false>(p, q, k, v, o, items, n_items, max_items, s, nullptr, split_acc);
       else st = f32 ? launch_fwd<128, false, true>(p, q, k, v, o, items, n_items, max_items, s)
-                    : launch_fwd<128, false, false>(p, q, k, v, o, items, n_items, max_items, s);
+                    : launch_fwd<128, false, false>(p, q, k, v, o, items, n_items, max_items, s, nullptr, split_acc);
     }
+  }
+  if (st == SIGATTN_OK && G) {   // sum the pieces of the split tail items into their O rows
+    if (p->dtype == SIGATTN_BF16)
+      fwd_split_finalize_kernel<true><<<G, 256, 0, s>>>(split_acc, split_map, n_split, reinterpret_cast<uint16_t*>(o),
+                                                        p->H, p->Nq, p->d, p->seqlens_q, layout_bshd(p) ? 1 : 0);
+    else
+      fwd_split_finalize_kernel<false><<<G, 256, 0, s>>>(split_acc, split_map, n_split, reinterpret_cast<uint16_t*>(o),
+                                                         p->H, p->Nq, p->d, p->seqlens_q, layout_bshd(p) ? 1 : 0);
+    count_launch();
+    CUDA_TRY(cudaGetLastError());
   }
   return st;
 }

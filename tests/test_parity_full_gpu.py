@@ -154,3 +154,27 @@ def test_c1_full_oracle_bench_launch():
     sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b, dq=dq, dk=dk, dv=dv, workspace=ws)
     torch.cuda.synchronize()
     check_full(cfg, q, k, v, do, o, (dq, dk, dv), alpha, b, tag="C1")
+
+
+@pytest.mark.parametrize("layout", ["bhsd", "bshd"])
+def test_tail_split_full_oracle(layout):
+    """d = 128 uniformly padded batch (B=2 H=16 N=8192, n = 6144): 768 equal two-tile items of 48 key
+    tiles are 5 full rounds of 148 CTAs plus 28, which the work list cuts along their key range into
+    5 pieces each (sched.cuh split_tail_block; additivity over key blocks); the pieces' fp32
+    partials are summed by fwd_split_finalize_kernel.  Every O element vs the full oracle, padded
+    rows exact 0."""
+    import paper_2604_27124_b200 as sa
+    cfg = I.Config("tail_split_d128", B=2, H=16, N=8192, d=128, lengths=[6144] * 2, seed=61)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    alpha, b = 1.0 / math.sqrt(cfg.d), -math.log(cfg.N)
+    fws = torch.empty(sa.fwd_workspace_bytes(cfg.B, cfg.H, cfg.N, cfg.N, cfg.d), dtype=torch.uint8, device="cuda")
+    if layout == "bshd":
+        qt, kt, vt = (t.transpose(1, 2).contiguous() for t in (q, k, v))
+        o = sa.sigattn_fwd(qt, kt, vt, nq, nk, alpha, b, out=torch.full_like(qt, float("nan")), layout="bshd",
+                           workspace=fws).transpose(1, 2)
+    else:
+        o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b, out=torch.full_like(q, float("nan")), workspace=fws)
+    torch.cuda.synchronize()
+    n_split = int(fws.view(torch.int32)[1].item())
+    assert torch.cuda.get_device_properties(0).multi_processor_count != 148 or n_split == 28, n_split
+    check_full(cfg, q, k, v, do, o, None, alpha, b, tag=f"tail split {layout} ({n_split} split items)")
