@@ -687,11 +687,11 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     if (kDQ && threadIdx.x == kEpiThread0) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
   }
 
-  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill) {   // padded dK / dV rows no tile epilogue writes
-    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0, args.fill_pad);
-    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0, args.fill_pad);
+  if (!SIGATTN_DBG_NOFILL && (warp == C::kWarpFill || warp == C::kWarpAlloc)) {   // padded dK / dV rows no tile epilogue writes
+    pad_fill_warp(args.dk, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0, args.fill_pad, warp == C::kWarpFill ? 0 : 1, 2);
+    pad_fill_warp(args.dv, D * 2, args.B, args.H, args.Nk, args.seqlens_k, args.seqlens_q, args.Nq, kTile, lane, kBSHD ? 1 : 0, args.fill_pad, warp == C::kWarpFill ? 0 : 1, 2);
     if (args.dq_pad)   // dq_finalize_kernel covers the rows below
-      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, kBSHD ? 1 : 0, args.fill_pad);
+      pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, kBSHD ? 1 : 0, args.fill_pad, warp == C::kWarpFill ? 0 : 1, 2);
   }
 
   sm100::tc_fence_before();

@@ -331,9 +331,9 @@ sigattn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     }
   }
 
-  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill)   // padded dQ rows beyond the last valid tile
+  if (!SIGATTN_DBG_NOFILL && (warp == C::kWarpFill || warp == C::kWarpAlloc))   // padded dQ rows beyond the last valid tile
     pad_fill_warp(args.dq, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
-                  kTile, lane, kBSHD ? 1 : 0, args.fill_pad);
+                  kTile, lane, kBSHD ? 1 : 0, args.fill_pad, warp == C::kWarpFill ? 0 : 1, 2);
 
   sm100::tc_fence_before();
   __syncthreads();

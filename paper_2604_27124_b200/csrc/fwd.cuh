@@ -459,9 +459,9 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
   }
 
-  if (!SIGATTN_DBG_NOFILL && warp == C::kWarpFill && args.o)   // padded O rows beyond the last valid tile
+  if (!SIGATTN_DBG_NOFILL && (warp == C::kWarpFill || warp == C::kWarpAlloc) && args.o)   // padded O rows beyond the last valid tile
     pad_fill_warp(args.o, D * (kOutF32 ? 4 : 2), args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk,
-                  128, lane, args.bshd, args.fill_pad);
+                  128, lane, args.bshd, args.fill_pad, warp == C::kWarpFill ? 0 : 1, 2);
 
   if (kOutF32 && args.peer_o) sm100::fence_sys();   // this CTA's peer reductions before kernel completion
   sm100::tc_fence_before();

@@ -186,15 +186,19 @@ __device__ __forceinline__ size_t row_off(int bshd, int H, int N, int D, int b, 
 //   pad_rows = 0 (SIGATTN_F_NO_ZERO_PAD_OUT: padded rows are left as they are): only the VALID rows
 //                 no epilogue writes, [0, n_own) of a sequence with n_other == 0 -- an empty key (or
 //                 query) set gives exact-zero valid outputs (empty sums, Eq. 2).
-// Slabs are strided over the grid; the idle warp of each persistent attention CTA runs this
-// alongside the main work.
+// The rows of every slab are spread over all workers -- the grid's CTAs times the `nworkers` idle
+// warps of each persistent attention CTA (worker `k` of this CTA) -- in round-robin 512-byte blocks,
+// so a batch whose padding sits in a few long sequences (C3: 74% padding) is zeroed evenly by every
+// SM alongside the main work instead of by the few CTAs that own those slabs.
 __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, int H, int N,
                                               const int32_t* __restrict__ lens_own,
                                               const int32_t* __restrict__ lens_other, int N_other, int gran,
-                                              uint32_t lane, int bshd = 0, int pad_rows = 1) {
+                                              uint32_t lane, int bshd = 0, int pad_rows = 1, int k = 0,
+                                              int nworkers = 1) {
   const uint4 z = make_uint4(0, 0, 0, 0);
   const int cpr = row_bytes / 16;   // 16-byte chunks per row
-  for (int zh = blockIdx.x; zh < B * H; zh += gridDim.x) {
+  const long long W = (long long)gridDim.x * nworkers, w = (long long)blockIdx.x * nworkers + k;
+  for (int zh = 0; zh < B * H; ++zh) {
     const int b = zh / H, h = zh - b * H;
     const int n = clamp_len(lens_own, b, N), m = clamp_len(lens_other, b, N_other);
     int r0, r1;
@@ -206,17 +210,18 @@ __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, i
       r1 = m == 0 ? n : 0;
     }
     if (r0 >= r1) continue;
+    const long long total = (long long)(r1 - r0) * cpr;
     if (!bshd) {
-      const long long total = (long long)(r1 - r0) * cpr;
       uint4* base = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out) + ((size_t)zh * N + r0) * row_bytes);
-      for (long long i = lane; i < total; i += 32) base[i] = z;
+      for (long long i = w * 32 + lane; i < total; i += W * 32) base[i] = z;
     } else {
-      // row r of slab (b, h) starts at ((b N + r) H + h) row_bytes; cpr divides 32 (row_bytes is
-      // 128, 256 or 512): each lane owns one 16-byte chunk of every (32 / cpr)-th row
+      // row r of slab (b, h) starts at ((b N + r) H + h) row_bytes
       uint8_t* base = reinterpret_cast<uint8_t*>(out) + ((size_t)b * N * H + h) * row_bytes;
       const size_t rs = (size_t)H * row_bytes;
-      const int step = 32 / cpr, lr = (int)lane / cpr, c = (int)lane % cpr;
-      for (int r = r0 + lr; r < r1; r += step) reinterpret_cast<uint4*>(base + (size_t)r * rs)[c] = z;
+      for (long long i = w * 32 + lane; i < total; i += W * 32) {
+        const long long r = r0 + i / cpr, c = i % cpr;
+        reinterpret_cast<uint4*>(base + (size_t)r * rs)[c] = z;
+      }
     }
   }
 }
