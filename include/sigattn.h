@@ -140,7 +140,9 @@ int64_t sigattn_valid_flops(int B, int H, int d, const int32_t* host_nq, const i
  * q-tiles 2t and 2t+1), cost = key tiles -- the two-tile forward) or backward (kind = 1, items =
  * (b,h,k-tile), cost = query tiles) kernel visits, in visiting order (longest first, ties by
  * b then h then tile).  Each item is 4 int32: {b, h, tile, cost}.  Returns the item count, or
- * -1 on bad arguments; writes at most max_items.  tile = 128 rows.                            */
+ * -1 on bad arguments; writes at most max_items.  tile = 128 rows.  (The device list of the
+ * two-tile forward additionally cuts the items of a short last round of the persistent grid along
+ * their key range -- sched.cuh split_tail_block; this mirror returns the uncut list.)           */
 int64_t sigattn_worklist_host(int kind, int B, int H, int Nq, int Nk, const int32_t* host_nq,
                               const int32_t* host_nk, int32_t* items, int64_t max_items);
 
