@@ -99,6 +99,17 @@ struct BwdCfg {
 };
 
 
+// Query tile visited at step i of key tile kt's sweep: odd key tiles sweep backwards, so the CTAs of
+// one (b, h) split into two streams that meet in the middle instead of all reduce-adding their dQ
+// partials into the same query tile at the same time (L2 atomics on the same lines serialise);
+// each stream still shares its Q / dO tiles in L2.
+#ifndef SIGATTN_BWD_ALT_SWEEP
+#define SIGATTN_BWD_ALT_SWEEP 1
+#endif
+__device__ __forceinline__ int sweep_tile(int kt, int i, int nqt) {
+  return (SIGATTN_BWD_ALT_SWEEP && (kt & 1)) ? nqt - 1 - i : i;
+}
+
 // Walks this CTA's non-empty work items (first_item / next_item order) and their query tiles.
 struct TileIter {
   int it, n_items, i, nqt;
@@ -294,8 +305,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             sm100::mbar_arrive(&qdo_full[st]);
           } else {
             sm100::mbar_arrive_expect_tx(&qdo_full[st], 2 * C::kTileBytes);
-            sm100::tma_load_bh(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, i * kTile, zh, pol_q, kBSHD ? args.H : 0);
-            sm100::tma_load_bh(smem + C::kDOOff + st * C::kTileBytes, &tmDO, &qdo_full[st], 0, i * kTile, zh, pol_q, kBSHD ? args.H : 0);
+            const int qi = sweep_tile(kt, i, nqt);
+            sm100::tma_load_bh(smem + C::kQOff + st * C::kTileBytes, &tmQ, &qdo_full[st], 0, qi * kTile, zh, pol_q, kBSHD ? args.H : 0);
+            sm100::tma_load_bh(smem + C::kDOOff + st * C::kTileBytes, &tmDO, &qdo_full[st], 0, qi * kTile, zh, pol_q, kBSHD ? args.H : 0);
           }
         }
         __syncwarp();
@@ -512,7 +524,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           sm100::tmem_wait_ld_dep16(dp);
           // valid query columns here; the masked variant is chosen warp-uniformly (it also zeroes the
           // rows of padded keys)
-          const int ncol = nq - (i * kTile + qh * 64 + (int)w4 * 16);
+          const int ncol = nq - (sweep_tile(kt, i, nqt) * kTile + qh * 64 + (int)w4 * 16);
           uint32_t pp[8], dd[8];
           if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB, SIGATTN_BWD64_SPEC>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
           else bwd_row16<true, kBf16, kDB, SIGATTN_BWD64_SPEC>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
@@ -637,7 +649,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         if (pend) drain_dq(t - 1, pend_zh, pend_i);
         pend = true;
         pend_zh = (int)zh;
-        pend_i = i;
+        pend_i = sweep_tile(kt, i, nqt);
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
       sm100::mbar_wait_backoff(acc_full, item_c & 1);
