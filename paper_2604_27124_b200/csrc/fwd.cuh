@@ -126,12 +126,33 @@ template <bool kMask, bool kBf16>
 __device__ __forceinline__ void sigmoid_chunk32(uint32_t taddr, float (&v)[32], uint32_t (&pk)[16], float a, float c,
                                                 bool row_valid, int nvalid, bool& spec) {
 #if SIGATTN_FWD_SPEC
-  bool done = false;
   if (spec) {
-    done = sigma_row_spec4<32, kMask>(v, a, c, row_valid, nvalid);
-    if (!done) sm100::tmem_ld32_sync(taddr, v);
+    // t = x log2 e and the max of the valid t; the tier-4 sigma of every element packed straight to
+    // 16 bits (the scores are dead afterwards, so the MUFU ex2 and the FMA-pipe work interleave
+    // freely); the vote only decides whether to redo the chunk from the scores, reloaded from TMEM
+    float m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      ffma2(v[e], v[e + 1], v[e], v[e + 1], a, a, c, c);
+      if constexpr (kMask)
+        m = fmax3(m, e < nvalid ? v[e] : -INFINITY, e + 1 < nvalid ? v[e + 1] : -INFINITY);
+      else
+        m = fmax3(m, v[e], v[e + 1]);
+    }
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float p0, p1;
+      sigma2_fast4(v[e], v[e + 1], p0, p1);
+      if constexpr (kMask) {
+        p0 = (e < nvalid) ? p0 : 0.0f;
+        p1 = (e + 1 < nvalid) ? p1 : 0.0f;
+      }
+      pk[e >> 1] = sm100::pack2<kBf16>(p0, p1);
+    }
+    if (__all_sync(0xffffffffu, !row_valid || m <= kFastT4)) return;
+    sm100::tmem_ld32_sync(taddr, v);   // rare: some valid logit > -4
   }
-  if (!done) spec = sigma_row<32, kMask, 0>(v, a, c, row_valid, nvalid) == 4;   // one inlined copy
+  spec = sigma_row<32, kMask, 0>(v, a, c, row_valid, nvalid) == 4;
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
     float p0 = v[e], p1 = v[e + 1];
