@@ -48,6 +48,9 @@
 #ifndef SIGATTN_BWD_SPEC
 #define SIGATTN_BWD_SPEC 1        // tier-4 sigma evaluated before the warp vote (sigma_row_spec4)
 #endif
+#ifndef SIGATTN_BWD_SPEC_V2
+#define SIGATTN_BWD_SPEC_V2 1     // speculative tier 4 without the ordering barrier (sigmoid_chunk32 style)
+#endif
 #ifndef SIGATTN_BWD64_SPEC
 #define SIGATTN_BWD64_SPEC false  // ... in the d = 64 fused backward: vote first measured 1.5-8% faster
 #endif
@@ -156,15 +159,29 @@ __device__ __forceinline__ void bwd_sigma16(float (&v)[16], float a2, float b2, 
     return;
   }
 #if SIGATTN_BWD_SPEC
-  bool done = false;
   if (spec) {
-    done = sigma_row_spec4<16, kMask>(v, a2, b2, key_valid, nvalid);   // v: scores in, P out
-    if (!done) {
-      sm100::tmem_ld16(s_taddr, v);
-      sm100::tmem_wait_ld_dep16(v);
+#if SIGATTN_BWD_SPEC_V2
+    // scale, max and the tier-4 sigma in place with no ordering barrier; the vote only gates a
+    // reload-and-redo (as in the forward's sigmoid_chunk32)
+    float m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 16; e += 2) {
+      ffma2(v[e], v[e + 1], v[e], v[e + 1], a2, a2, b2, b2);
+      if constexpr (kMask)
+        m = fmax3(m, e < nvalid ? v[e] : -INFINITY, e + 1 < nvalid ? v[e + 1] : -INFINITY);
+      else
+        m = fmax3(m, v[e], v[e + 1]);
     }
+#pragma unroll
+    for (int e = 0; e < 16; e += 2) sigma2_fast4(v[e], v[e + 1], v[e], v[e + 1]);
+    if (__all_sync(0xffffffffu, !key_valid || m <= kFastT4)) return;
+#else
+    if (sigma_row_spec4<16, kMask>(v, a2, b2, key_valid, nvalid)) return;   // v: scores in, P out
+#endif
+    sm100::tmem_ld16(s_taddr, v);   // rare: some valid logit > -4
+    sm100::tmem_wait_ld_dep16(v);
   }
-  if (!done) spec = sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid) == 4;   // one inlined copy
+  spec = sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid) == 4;   // one inlined copy
 #else
   (void)s_taddr;
   (void)spec;
