@@ -314,15 +314,84 @@ void run_w(int warps, long long* cyc, uint32_t* sink, float bias2) {
          (double)warps * 32 * kW * iters / c);
 }
 
+
+// instruction-class ablation of the tier-4 chunk path (16 warps): which part limits it
+template <int kVar>
+__global__ void __launch_bounds__(1024, 1) kern_ab(int iters, long long* cyc, uint32_t* sink, float bias2) {
+  __shared__ uint32_t tmem_holder;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0) sm100::tmem_alloc<512>(&tmem_holder);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_holder;
+  const uint32_t lane_addr = ((warp & 3) * 32) << 16;
+  const uint32_t col = (warp >> 2) * 64;
+  {
+    uint32_t v[16];
+    for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(((lane * 7 + i * 13) % 31 - 15) * 0.5f);
+    sm100::tmem_st16(tmem + lane_addr + col, v);
+    sm100::tmem_st16(tmem + lane_addr + col + 16, v);
+    sm100::tmem_wait_st();
+  }
+  __syncthreads();
+  uint32_t acc = 0;
+  const float a2 = 0.125f * 1.4426950408889634f;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float r[32];
+    uint32_t pk[16];
+    sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+    float m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      if (kVar != 3) ffma2(r[e], r[e + 1], r[e], r[e + 1], a2, a2, bias2, bias2);
+      if (kVar != 1) m = fmax3(m, r[e], r[e + 1]);
+    }
+    bool ok = (kVar == 1) ? true : __all_sync(0xffffffffu, m <= kFastT4);
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float p0, p1;
+      const float u0 = ex2_ftz(r[e]), u1 = ex2_ftz(r[e + 1]);
+      if (kVar == 4) { p0 = u0; p1 = u1; }
+      else ffma2(p0, p1, u0, u1, -u0, -u1, u0, u1);
+      if (kVar == 2) pk[e >> 1] = __float_as_uint(p0) ^ __float_as_uint(p1);
+      else pk[e >> 1] = sm100::pack2<true>(p0, p1);
+    }
+    if (!ok) pk[0] ^= 1;
+    sm100::tmem_st16(tmem + lane_addr + col + 32, pk);
+    if ((it & 3) == 3) sm100::tmem_wait_st();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc ^= pk[i];
+  }
+  long long t1 = clock64();
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc<512>(tmem);
+}
+template <int kVar>
+void run_ab(const char* name, long long* cyc, uint32_t* sink, float bias2) {
+  const int iters = 4000, warps = 16;
+  kern_ab<kVar><<<148, warps * 32>>>(iters, cyc, sink, bias2);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return; }
+  long long c;
+  cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("  ablation %-40s %6.2f elem/clk/SM\n", name, (double)warps * 32 * 32 * iters / c);
+}
+
 int main() {
   long long* cyc;
   uint32_t* sink;
   cudaMalloc(&cyc, 148 * 8);
   cudaMalloc(&sink, 148 * 512 * 4);
   const float b4 = -13.0f, b0 = 0.0f;   // t = s a2 + b2: tier 4 (b = -log 8192 -> b2 ~ -13) / exact tier
-  for (int w : {8, 16, 24, 32}) {
-    run_w<32>(w, cyc, sink, b4);
-    run_w<16>(w, cyc, sink, b4);
-  }
+  run_ab<0>("full tier-4 path", cyc, sink, b4);
+  run_ab<1>("no max / vote", cyc, sink, b4);
+  run_ab<2>("no bf16 pack (F2FP)", cyc, sink, b4);
+  run_ab<3>("no scale FFMA2", cyc, sink, b4);
+  run_ab<4>("no sigma FFMA2 (p = u)", cyc, sink, b4);
   return 0;
 }
