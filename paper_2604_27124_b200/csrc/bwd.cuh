@@ -54,6 +54,12 @@
 #ifndef SIGATTN_BWD64_SPEC
 #define SIGATTN_BWD64_SPEC false  // ... in the d = 64 fused backward: vote first measured 1.5-8% faster
 #endif
+// 1: the compute warps store their packed dS^T straight into the swizzled smem operand of the dQ MMA
+// (beside the TMEM store): no TMEM read-back by the epilogue, no ds_copied hand-off in front of the
+// next tile's score MMAs.  0: the epilogue warpgroup stages dS^T from TMEM.
+#ifndef SIGATTN_BWD_DS_DIRECT
+#define SIGATTN_BWD_DS_DIRECT 1
+#endif
 namespace sigattn {
 
 struct BwdArgs {
@@ -412,7 +418,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t b2 = tq & 1;
 #if !SIGATTN_DBG_MMAONLY
       sm100::mbar_wait(dq_empty, (tq & 1) ^ 1);                  // epilogue drained the accumulator
-      sm100::mbar_wait(&ds_full[b2], (tq >> 1) & 1);             // dS(tq) staged in smem, proxy-fenced
+      if (!SIGATTN_BWD_DS_DIRECT)   // (direct: p_full of both halves, waited above, covers the stores)
+        sm100::mbar_wait(&ds_full[b2], (tq >> 1) & 1);           // dS(tq) staged in smem, proxy-fenced
 #endif
       if (lane == 0 && tq >= 40 && tq < 48) sm100::trace_event(args.trace, 3328 + (tq - 40) * 8 + 3, 4094);
       sm100::tc_fence_after();
@@ -456,7 +463,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
         MMA_TR(6);
 #if !SIGATTN_DBG_MMAONLY
-        if (kDQ) sm100::mbar_wait(&ds_copied[0], t & 1);   // dS^T(t, q0) left TMEM before S/dP(t+1, q0) land there
+        if (kDQ && !SIGATTN_BWD_DS_DIRECT) sm100::mbar_wait(&ds_copied[0], t & 1);   // dS^T(t, q0) left TMEM before S/dP(t+1, q0) land there
 #endif
         MMA_TR(7);
         sm100::tc_fence_after();
@@ -484,7 +491,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       MMA_TR(1);
       if (nxt.valid) {
 #if !SIGATTN_DBG_MMAONLY
-        if (kDQ) sm100::mbar_wait(&ds_copied[1], t & 1);
+        if (kDQ && !SIGATTN_BWD_DS_DIRECT) sm100::mbar_wait(&ds_copied[1], t & 1);
 #endif
         sm100::tc_fence_after();
         if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 1);
@@ -505,6 +512,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
+    const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
+    (void)ds_row;
     uint32_t t = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
@@ -550,6 +559,15 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           // warpgroup stages dS^T into shared memory for the dQ MMA
           sm100::tmem_st8(tmem + lane_addr + s_col, pp);
           sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
+          if (kDQ && SIGATTN_BWD_DS_DIRECT) {
+            // queries [64 qh + 16 w4, +16) of key row `row` = 16-byte chunks 2 w4, 2 w4 + 1 of the
+            // half's 128-byte row, SW128 swizzle (chunk c at slot c ^ (row & 7))
+            if (qh == 0) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) MMA done with the buffer
+            const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes + qh * (kTile * 128);
+            sm100::st_shared_v4(dsr + (((2 * w4) ^ (row & 7)) * 16), dd[0], dd[1], dd[2], dd[3]);
+            sm100::st_shared_v4(dsr + (((2 * w4 + 1) ^ (row & 7)) * 16), dd[4], dd[5], dd[6], dd[7]);
+            sm100::fence_proxy_async_smem();
+          }
           sm100::tmem_wait_st();
           sm100::tc_fence_before();
           __syncwarp();
@@ -633,6 +651,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const size_t zh = (size_t)(b * args.H + h);
       for (int i = 0; i < nqt * kDQ; ++i, ++t) {
+        if (SIGATTN_BWD_DS_DIRECT) {   // no staging: drain dQ(t) as soon as it lands
+          drain_dq(t, (int)zh, sweep_tile(kt, i, nqt));
+          continue;
+        }
         const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
 #pragma unroll 1
         for (int qh = 0; qh < 2; ++qh) {

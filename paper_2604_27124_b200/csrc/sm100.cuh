@@ -21,6 +21,7 @@ __device__ __forceinline__ void trace_globaltime(long long* buf, int slot) {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   if (buf) buf[(size_t)blockIdx.x * 4096 + slot] = t;
+  if (buf) buf[(size_t)blockIdx.x * 4096 + slot - 2] = clock64();   // slots 4092 / 4093: SM clock
 #endif
 }
 __device__ __forceinline__ void trace_event(long long* buf, int slot, int limit) {

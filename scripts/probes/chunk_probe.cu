@@ -352,7 +352,10 @@ __global__ void __launch_bounds__(1024, 1) kern_ab(int iters, long long* cyc, ui
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
       float p0, p1;
-      const float u0 = ex2_ftz(r[e]), u1 = ex2_ftz(r[e + 1]);
+      float u0, u1;
+      constexpr int kEmuK = kVar >= 5 ? kVar - 3 : 0;   // kVar 5..: pair e/2 % k == k/2 on the FMA pipe
+      if (kEmuK > 0 && ((e >> 1) % (kEmuK > 0 ? kEmuK : 1)) == kEmuK / 2) exp2_fma2(r[e], r[e + 1], u0, u1);
+      else { u0 = ex2_ftz(r[e]); u1 = ex2_ftz(r[e + 1]); }
       if (kVar == 4) { p0 = u0; p1 = u1; }
       else ffma2(p0, p1, u0, u1, -u0, -u1, u0, u1);
       if (kVar == 2) pk[e >> 1] = __float_as_uint(p0) ^ __float_as_uint(p1);
@@ -393,5 +396,10 @@ int main() {
   run_ab<2>("no bf16 pack (F2FP)", cyc, sink, b4);
   run_ab<3>("no scale FFMA2", cyc, sink, b4);
   run_ab<4>("no sigma FFMA2 (p = u)", cyc, sink, b4);
+  run_ab<5>("exp2 on FMA pipe, 1 pair in 2", cyc, sink, b4);
+  run_ab<6>("exp2 on FMA pipe, 1 pair in 3", cyc, sink, b4);
+  run_ab<7>("exp2 on FMA pipe, 1 pair in 4", cyc, sink, b4);
+  run_ab<8>("exp2 on FMA pipe, 1 pair in 5", cyc, sink, b4);
+  run_ab<11>("exp2 on FMA pipe, 1 pair in 8", cyc, sink, b4);
   return 0;
 }

@@ -2,8 +2,8 @@
 #include <cstdio>
 #include "sm100.cuh"
 
-template <int MODE>   // 0: ld32, 1: ld16, 2: st16, 3: ld32 x4 in flight
-__global__ void __launch_bounds__(512, 1) probe(long long* out, int iters) {
+template <int MODE>   // 0: ld32, 1: ld16, 2: st16, 3: ld32 x2 in flight, 4: ld32 + ld32 of a second lane block wait once
+__global__ void __launch_bounds__(1024, 1) probe(long long* out, int iters) {
   __shared__ uint32_t tmem_holder;
   const int warp = threadIdx.x / 32;
   if (warp == 0) sm100::tmem_alloc<512>(&tmem_holder);
@@ -12,7 +12,7 @@ __global__ void __launch_bounds__(512, 1) probe(long long* out, int iters) {
   sm100::tc_fence_after();
   const uint32_t tmem = tmem_holder;
   const uint32_t lane_addr = ((warp & 3) * 32) << 16;
-  const uint32_t col = (warp >> 2) * 32;
+  const uint32_t col = ((warp >> 2) * 32) & 127;
   uint32_t acc = 0;
   __syncthreads();
   long long t0 = clock64();
@@ -34,8 +34,8 @@ __global__ void __launch_bounds__(512, 1) probe(long long* out, int iters) {
       acc += 1;
     } else {
       uint32_t a[32], b[32];
-      sm100::tmem_ld32(tmem + lane_addr + col + (it & 1) * 128, a);
-      sm100::tmem_ld32(tmem + lane_addr + col + 256 + (it & 1) * 128, b);
+      sm100::tmem_ld32(tmem + lane_addr + (col & 127) + (it & 1) * 128, a);
+      sm100::tmem_ld32(tmem + lane_addr + (col & 127) + 256 + (it & 1) * 128, b);
       sm100::tmem_wait_ld_dep(a);
       sm100::tmem_wait_ld_dep(b);
       for (int i = 0; i < 32; ++i) acc += a[i] ^ b[i];
@@ -57,7 +57,7 @@ int main() {
   const char* names[4] = {"ld 32x32b.x32 (4 KB/warp)", "ld 32x32b.x16 (2 KB/warp)", "st 32x32b.x16 (2 KB/warp)",
                           "2 x ld.x32 in flight (8 KB/warp)"};
   const double bytes[4] = {4096, 2048, 2048, 8192};
-  for (int threads : {128, 256, 512}) {
+  for (int threads : {128, 256, 512, 1024}) {
     for (int m = 0; m < 4; ++m) {
       void (*k)(long long*, int) = m == 0 ? probe<0> : m == 1 ? probe<1> : m == 2 ? probe<2> : probe<3>;
       k<<<148, threads>>>(d, iters);
