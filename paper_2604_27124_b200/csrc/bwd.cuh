@@ -745,6 +745,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       pad_fill_warp(args.dq_pad, D * 2, args.B, args.H, args.Nq, args.seqlens_q, args.seqlens_k, args.Nk, kTile, lane, kBSHD ? 1 : 0, args.fill_pad, warp == C::kWarpFill ? 0 : 1, 2);
   }
 
+  if (lane == 0) sm100::trace_event(args.trace, 4064 + (int)warp, 4092);   // per-warp end (trace builds)
   sm100::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) sm100::trace_globaltime(args.trace, 4095);

@@ -198,9 +198,14 @@ __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, i
   const uint4 z = make_uint4(0, 0, 0, 0);
   const int cpr = row_bytes / 16;   // 16-byte chunks per row
   const long long W = (long long)gridDim.x * nworkers, w = (long long)blockIdx.x * nworkers + k;
-  // 32 slabs per step, one per lane: the sequence lengths of a step are loaded in parallel (a serial
-  // walk paid two dependent global loads per slab -- 60 us of a 130 us forward at B H = 512); a
-  // ballot then hands the slabs with rows to zero to the whole warp, one at a time.
+  // The 16-byte chunks to zero, concatenated over the slabs in (b, h) order, are cut into 512-byte
+  // blocks dealt round-robin to the W workers.  A step covers 32 slabs, one per lane: lengths loaded
+  // in parallel, chunk counts prefix-summed across the warp, and each lane tests whether this
+  // worker owns a block reaching into its slab; the warp then stores only into those slabs.  (A walk
+  // over every slab by every worker cost ~100 clk per slab: 60-140 us past the main work at
+  // B H = 512-1024.)  Rows are a power of two of chunks, so no division in the store loop.
+  const int lg = __ffs(cpr) - 1;
+  long long run = 0;   // chunks of the earlier steps
   for (int zh0 = 0; zh0 < B * H; zh0 += 32) {
     const int zl = zh0 + (int)lane;
     int r0 = 0, r1 = 0;
@@ -214,27 +219,38 @@ __device__ __forceinline__ void pad_fill_warp(void* out, int row_bytes, int B, i
         r0 = 0;
         r1 = m == 0 ? n : 0;
       }
+      r1 = max(r1, r0);
     }
-    unsigned todo = __ballot_sync(0xffffffffu, r0 < r1);
+    const long long c = (long long)(r1 - r0) << lg;
+    long long incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    const long long lo = run + incl - c, hi = run + incl;   // this lane's slab: global chunks [lo, hi)
+    const long long b0 = lo >> 5;
+    const long long bw = b0 + ((w - b0 % W) % W + W) % W;   // this worker's first block at or after b0
+    unsigned todo = __ballot_sync(0xffffffffu, c > 0 && (bw << 5) < hi);
     while (todo) {
-      const int src = __ffs(todo) - 1;
+      const int sl = __ffs(todo) - 1;
       todo &= todo - 1;
-      const int zh = zh0 + src, b = zh / H, h = zh - b * H;
-      const int a0 = __shfl_sync(0xffffffffu, r0, src), a1 = __shfl_sync(0xffffffffu, r1, src);
-      const long long total = (long long)(a1 - a0) * cpr;
-      if (!bshd) {
-        uint4* base = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out) + ((size_t)zh * N + a0) * row_bytes);
-        for (long long i = w * 32 + lane; i < total; i += W * 32) base[i] = z;
-      } else {
-        // row r of slab (b, h) starts at ((b N + r) H + h) row_bytes
-        uint8_t* base = reinterpret_cast<uint8_t*>(out) + ((size_t)b * N * H + h) * row_bytes;
-        const size_t rs = (size_t)H * row_bytes;
-        for (long long i = w * 32 + lane; i < total; i += W * 32) {
-          const long long r = a0 + i / cpr, c = i % cpr;
-          reinterpret_cast<uint4*>(base + (size_t)r * rs)[c] = z;
+      const long long slo = __shfl_sync(0xffffffffu, lo, sl), shi = __shfl_sync(0xffffffffu, hi, sl);
+      const long long sbw = __shfl_sync(0xffffffffu, bw, sl);
+      const int a0 = __shfl_sync(0xffffffffu, r0, sl);
+      const int zh = zh0 + sl, b = zh / H, h = zh - b * H;
+      uint8_t* slab = reinterpret_cast<uint8_t*>(out) +
+                      (bshd ? ((size_t)b * N * H + h) * row_bytes : ((size_t)zh * N + a0) * row_bytes);
+      for (long long blk = sbw; (blk << 5) < shi; blk += W) {
+        const long long g = (blk << 5) + lane;
+        if (g >= slo && g < shi) {
+          const long long i = g - slo;
+          if (!bshd) reinterpret_cast<uint4*>(slab)[i] = z;
+          else reinterpret_cast<uint4*>(slab + ((size_t)(a0 + (i >> lg)) * H) * row_bytes)[i & (cpr - 1)] = z;
         }
       }
     }
+    run = __shfl_sync(0xffffffffu, hi, 31);
   }
 }
 

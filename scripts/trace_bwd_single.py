@@ -22,9 +22,16 @@ import paper_2604_27124_b200 as sa  # noqa: E402
 from paper_2604_27124_b200 import _lib, inputs as I  # noqa: E402
 
 w = sys.argv[1] if len(sys.argv) > 1 else "c3"
-cfg = I.C3 if w == "c3" else I.c2(int(w.split(":")[1]), 64)
+if w == "c3":
+    cfg = I.C3
+else:   # c2:N[:pad]
+    parts = w.split(":")
+    cfg = I.c2(int(parts[1]), 64)
+    if len(parts) > 2:
+        n_ = int(round(cfg.N * (1 - float(parts[2]))))
+        cfg = I.Config(cfg.name + "_pad", B=cfg.B, H=cfg.H, N=cfg.N, d=64, lengths=[n_] * cfg.B, seed=0)
 q, k, v, do, nq, nk = I.make_inputs_gpu_fast(cfg, "cuda")
-alpha, b = 1 / 8, -math.log(cfg.N)
+alpha, b = 1 / 8, -math.log(max(cfg.nk))
 for _ in range(3):
     sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b)
 buf = torch.zeros(148 * 4096, dtype=torch.int64, device="cuda")
@@ -34,6 +41,22 @@ sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b)
 torch.cuda.synchronize()
 lib.sigattn_set_trace_buffer(None)
 T = buf.view(148, 4096).cpu().numpy().astype(np.float64)
+g0, g1 = T[:, 4094], T[:, 4095]
+ok = (g0 > 0) & (g1 > 0)
+mhz = (T[ok, 4093] - T[ok, 4092]) / (g1[ok] - g0[ok]) * 1e3
+print("CTA end (us after first start): min %.1f median %.1f max %.1f; SM clock %.0f MHz" % (
+    (g1[ok].min() - g0[ok].min()) / 1e3, np.median(g1[ok] - g0[ok].min()) / 1e3, (g1[ok].max() - g0[ok].min()) / 1e3,
+    np.median(mhz)))
+for cta in range(3):
+    r = T[cta]
+    nt = int((r[0:512] > 0).sum())
+    k0 = r[4092]
+    print("CTA %d: %d tiles, first p_full0 %d clk after start, last dQ issued %d, end %d" % (
+        cta, nt, r[0] - k0, r[1536 + nt - 1] - k0, r[4093] - k0))
+for cta in (0, 1, 40, 100):
+    r = T[cta]
+    print("CTA %3d warp end (k clk after start): " % cta + " ".join("%d:%.0f" % (w_, (r[4064 + w_] - r[4092]) / 1e3)
+                                                                for w_ in range(24) if r[4064 + w_] > 0))
 per, agg = [], {}
 for cta in range(148):
     r = T[cta]
