@@ -20,6 +20,7 @@
 // by sched.cuh from the device seqlens, so fully padded query tiles are never visited
 // and the key loop stops at ceil(n_k / 128) tiles.
 #pragma once
+#include <type_traits>
 #include "sched.cuh"
 #include "sigmoid.cuh"
 #include "sm100.cuh"
@@ -122,14 +123,27 @@ __device__ __forceinline__ void sigmoid_row32(float (&v)[32], uint32_t (&pk)[16]
 // evaluated speculatively before the warp vote; on a failed vote (some valid logit > -4, rare with
 // b = -log n) the scores are reloaded -- the chunk's S columns are not yet overwritten by P -- and
 // the exact tiers of sigma_row run.
-template <bool kMask, bool kBf16>
+// Speculative tier of sigmoid_chunk32, chosen per work item from the sequence's bias: with
+// b = -log n and logits alpha s of unit spread, some logit of a 32 x 32 chunk exceeds -4 in ~0.03% of
+// the chunks at n = 8192 (b = -9) but ~15% at n = 2048 (b = -7.6), and a failed speculation (reload +
+// exact redo) holds up the whole pair's P for that key tile.  Items with b <= kSpec4MaxBias speculate
+// the <= -4 tier (one FFMA2 per pair after the ex2), the others the <= -2 tier (three FMA-pipe ops
+// per pair).  Measured (d = 128): n = 2048 forward 0.31 -> 0.25 ms with the <= -2 tier, n = 8192
+// 0.91 -> 0.97 ms; the two tie at n = 4096 (b = -8.3).
+constexpr float kSpec4MaxBias = -8.3f;
+
+// 32 scores of one row (loaded from TMEM address taddr) -> 16 packed 16-bit P values.  SIGATTN_FWD_SPEC:
+// the kTier sigma is evaluated before the warp vote while `spec` holds (the last chunk of the warp
+// took a tier >= kTier); on a failed vote the scores are reloaded -- the chunk's S columns are not
+// yet overwritten by P -- and the exact tiers of sigma_row run.
+template <bool kMask, bool kBf16, int kTier>
 __device__ __forceinline__ void sigmoid_chunk32(uint32_t taddr, float (&v)[32], uint32_t (&pk)[16], float a, float c,
                                                 bool row_valid, int nvalid, bool& spec) {
 #if SIGATTN_FWD_SPEC
   if (spec) {
-    // t = x log2 e and the max of the valid t; the tier-4 sigma of every element packed straight to
-    // 16 bits (the scores are dead afterwards, so the MUFU ex2 and the FMA-pipe work interleave
-    // freely); the vote only decides whether to redo the chunk from the scores, reloaded from TMEM
+    // t = x log2 e and the max of the valid t; the speculative tier's sigma of every element packed
+    // straight to 16 bits (the scores are dead afterwards, so the MUFU ex2 and the FMA-pipe work
+    // interleave freely); the vote only decides whether to redo the chunk from the reloaded scores
     float m = -INFINITY;
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
@@ -142,17 +156,18 @@ __device__ __forceinline__ void sigmoid_chunk32(uint32_t taddr, float (&v)[32], 
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
       float p0, p1;
-      sigma2_fast4(v[e], v[e + 1], p0, p1);
+      if constexpr (kTier == 4) sigma2_fast4(v[e], v[e + 1], p0, p1);
+      else sigma2_fast(v[e], v[e + 1], p0, p1);
       if constexpr (kMask) {
         p0 = (e < nvalid) ? p0 : 0.0f;
         p1 = (e + 1 < nvalid) ? p1 : 0.0f;
       }
       pk[e >> 1] = sm100::pack2<kBf16>(p0, p1);
     }
-    if (__all_sync(0xffffffffu, !row_valid || m <= kFastT4)) return;
-    sm100::tmem_ld32_sync(taddr, v);   // rare: some valid logit > -4
+    if (__all_sync(0xffffffffu, !row_valid || m <= (kTier == 4 ? kFastT4 : kFastT))) return;
+    sm100::tmem_ld32_sync(taddr, v);   // rare: the speculative tier failed
   }
-  spec = sigma_row<32, kMask, 0>(v, a, c, row_valid, nvalid) == 4;
+  spec = sigma_row<32, kMask, 0>(v, a, c, row_valid, nvalid) >= kTier;
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
     float p0 = v[e], p1 = v[e + 1];
@@ -382,7 +397,7 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t row = quarter * 32 + lane;    // tile row = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
-    bool spec = true;                            // speculate tier 4 while the last chunk took it
+    bool spec = true;                            // speculate while the last chunk took the speculated tier
     uint32_t s_it = 0, c = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
@@ -393,37 +408,44 @@ sigattn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const float bias = args.bias_per_seq ? args.bias_per_seq[b] : args.bias;
       const float a2 = args.scale * kLog2e;    // t = x log2 e = s (alpha log2 e) + b log2 e
       const float b2 = bias * kLog2e;
+      const bool spec4 = bias <= kSpec4MaxBias;   // speculative sigma tier of this item
       const bool row_valid = qt * kTile + (int)row < nq;
-      for (int j = 0; j < nkt; ++j) {
-        const uint32_t si = s_it + j;
-        if ((si & 1) != pair) continue;          // the other warpgroup pair takes this key tile
-        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 3072 + si, 3584);
-        SIGATTN_COMPUTE_WAIT(&s_full[si % C::kSBuf], (si / C::kSBuf) & 1);
-        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 2048 + si, 2560);
-        sm100::tc_fence_after();
+      // the key loop, instantiated for the item's speculative sigma tier (one hot copy per item)
+      auto key_loop = [&](auto tier_c) {
+        constexpr int kT = decltype(tier_c)::value;
+        for (int j = 0; j < nkt; ++j) {
+          const uint32_t si = s_it + j;
+          if ((si & 1) != pair) continue;          // the other warpgroup pair takes this key tile
+          if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 3072 + si, 3584);
+          SIGATTN_COMPUTE_WAIT(&s_full[si % C::kSBuf], (si / C::kSBuf) & 1);
+          if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 2048 + si, 2560);
+          sm100::tc_fence_after();
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          const uint32_t col = (si % C::kSBuf) * 128 + gp * 64 + ch * 32;
-          const int nvalid = nk - (j * kTile + (int)gp * 64 + ch * 32);   // valid keys in these 32 columns
-          float r[32];
-          uint32_t pk[16];
-          sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
-#if SIGATTN_DBG_FWD_NOSIGMA   // timing experiments only: P = bits of S, no sigma work
+          for (int ch = 0; ch < 2; ++ch) {
+            const uint32_t col = (si % C::kSBuf) * 128 + gp * 64 + ch * 32;
+            const int nvalid = nk - (j * kTile + (int)gp * 64 + ch * 32);   // valid keys in these 32 columns
+            float r[32];
+            uint32_t pk[16];
+            sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+  #if SIGATTN_DBG_FWD_NOSIGMA   // timing experiments only: P = bits of S, no sigma work
 #pragma unroll
-          for (int e = 0; e < 16; ++e) pk[e] = __float_as_uint(r[2 * e]) ^ __float_as_uint(r[2 * e + 1]);
-#else
-          if (nvalid >= 32) sigmoid_chunk32<false, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
-          else sigmoid_chunk32<true, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
-#endif
-          // P over the first half of this warpgroup's 64 columns (chunk 0's columns are already read)
-          sm100::tmem_st16(tmem + lane_addr + (si % C::kSBuf) * 128 + gp * 64 + ch * 16, pk);
+            for (int e = 0; e < 16; ++e) pk[e] = __float_as_uint(r[2 * e]) ^ __float_as_uint(r[2 * e + 1]);
+  #else
+            if (nvalid >= 32) sigmoid_chunk32<false, kBf16, kT>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
+            else sigmoid_chunk32<true, kBf16, kT>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
+  #endif
+            // P over the first half of this warpgroup's 64 columns (chunk 0's columns are already read)
+            sm100::tmem_st16(tmem + lane_addr + (si % C::kSBuf) * 128 + gp * 64 + ch * 16, pk);
+          }
+          sm100::tmem_wait_st();
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&p_full[si % C::kSBuf]);
+          if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 2560 + si, 3072);
         }
-        sm100::tmem_wait_st();
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&p_full[si % C::kSBuf]);
-        if (lane == 0 && warp == pair * 8) sm100::trace_event(args.trace, 2560 + si, 3072);
-      }
+      };
+      if (spec4) key_loop(std::integral_constant<int, 4>{});
+      else key_loop(std::integral_constant<int, 2>{});
       // ---- epilogue, run by the pair that evaluated the item's last key tile (the other pair goes
       // straight on to the next item's first tile): O rows of this q tile, columns [gp D/2, +D/2)
       const uint32_t epi_pair = (s_it + nkt - 1) & 1;

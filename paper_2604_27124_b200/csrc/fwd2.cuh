@@ -17,6 +17,7 @@
 // ring), a pair's next S never waits for the other pair's P, which is what serialised sigma and
 // the MMAs there.
 #pragma once
+#include <type_traits>
 #include "fwd.cuh"
 
 namespace sigattn {
@@ -101,6 +102,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (threadIdx.x == 0) sm100::trace_globaltime(args.trace, 4094);
   const int n_items = *args.n_items;
   // tiles of this item that hold a valid query: A always, B when 2p + 1 < ceil(n_q / 128)
   auto has_b = [&](int b, int pi) {
@@ -185,7 +187,9 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
       if (args.counters && sm100::elect_one()) atomicAdd(args.counters, (unsigned long long)(ntq * nkt));
       __syncwarp();
       const uint32_t qb = c % C::kQBufs;
+      if (lane == 0) sm100::trace_event(args.trace, c, 512);                // item c: Q wait start
       sm100::mbar_wait(&q_full[qb], (c / C::kQBufs) & 1);
+      if (lane == 0) sm100::trace_event(args.trace, 512 + c, 1024);         // item c: Q ready
       // S_x(j) = Q_x K_j^T into slot x's buffer; the last S of key tile j releases K_j
       auto issue_s = [&](int x, int j) {
         const uint32_t kvi = kv_it + j, st = kvi % C::kStages;
@@ -235,6 +239,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         __syncwarp();
       };
       for (int x = 0; x < ntq; ++x) issue_s(x, 0);
+      if (lane == 0) sm100::trace_event(args.trace, 1024 + c, 1536);        // item c: first S issued
       if (nkt == 1) release_q();
       if constexpr (C::kSepP) {
         // events arrive as s_free_A(j), s_free_B(j), p_full_A(j), p_full_B(j): issue in that order
@@ -261,6 +266,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         for (int x = 0; x < ntq; ++x) sm100::mma_commit(&o_full[x]);
       }
       __syncwarp();
+      if (lane == 0) sm100::trace_event(args.trace, 1536 + c, 2048);        // item c: last PV issued
       for (int x = 0; x < ntq; ++x) ++xo[x];
       kv_it += nkt;
       ++c;
@@ -272,7 +278,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;
     const uint32_t lane_addr = (quarter * 32) << 16;
-    bool spec = true;   // speculate tier 4 while the last chunk took it
+    bool spec = true;   // speculate while the last chunk took the speculated tier
     uint32_t xs = 0, xo = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const Item2 item = decode(args.items[it]);
@@ -285,49 +291,58 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
       const float bias = args.bias_per_seq ? args.bias_per_seq[b] : args.bias;
       const float a2 = args.scale * kLog2e;
       const float b2 = bias * kLog2e;
+      const bool spec4 = bias <= kSpec4MaxBias;   // speculative sigma tier of this item
       const bool row_valid = qt * kTile + (int)row < nq;
-      for (int j = 0; j < nkt; ++j, ++xs) {
-        SIGATTN_COMPUTE_WAIT(&s_full[x], xs & 1);
-        sm100::tc_fence_after();
+      // the key loop, instantiated for the item's speculative sigma tier (one hot copy per item)
+      auto key_loop = [&](auto tier_c) {
+        constexpr int kT = decltype(tier_c)::value;
+        for (int j = 0; j < nkt; ++j, ++xs) {
+          SIGATTN_COMPUTE_WAIT(&s_full[x], xs & 1);
+          sm100::tc_fence_after();
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          const uint32_t col = x * 128 + gp * 64 + ch * 32;
-          const int nvalid = nk - ((kb + j) * kTile + (int)gp * 64 + ch * 32);
-          float r[32];
-          uint32_t pk[16];
-          sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
-          if (C::kSepP && ch == 1) {   // all of this warp's S_x(j) columns are read: release the buffer
-            sm100::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(&s_free[x]);
-          }
-          if (SIGATTN_DBG_FWD_NOSIGMA) {   // timing experiments only: P = bits of S, no sigma work
-#pragma unroll
-            for (int e = 0; e < 16; ++e) pk[e] = __float_as_uint(r[2 * e]) ^ __float_as_uint(r[2 * e + 1]);
-          } else if (C::kSepP) {   // S already released: no reload possible, vote-first tiers
-            if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
-            else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
-          } else {
-            if (nvalid >= 32) sigmoid_chunk32<false, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
-            else sigmoid_chunk32<true, kBf16>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
-          }
-          if (C::kSepP) {
-            if (ch == 0) {   // PV_x(j-1) has read the previous P_x
-              sm100::mbar_wait(&pv_done[x], (xs & 1) ^ 1);
-              sm100::tc_fence_after();
+          for (int ch = 0; ch < 2; ++ch) {
+            const uint32_t col = x * 128 + gp * 64 + ch * 32;
+            const int nvalid = nk - ((kb + j) * kTile + (int)gp * 64 + ch * 32);
+            float r[32];
+            uint32_t pk[16];
+            sm100::tmem_ld32_sync(tmem + lane_addr + col, r);
+            if (C::kSepP && ch == 1) {   // all of this warp's S_x(j) columns are read: release the buffer
+              sm100::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) sm100::mbar_arrive(&s_free[x]);
             }
-            sm100::tmem_st16(tmem + lane_addr + C::kColP + x * 64 + gp * 32 + ch * 16, pk);
-          } else {
-            sm100::tmem_st16(tmem + lane_addr + x * 128 + gp * 64 + ch * 16, pk);
+            if (SIGATTN_DBG_FWD_NOSIGMA) {   // timing experiments only: P = bits of S, no sigma work
+#pragma unroll
+              for (int e = 0; e < 16; ++e) pk[e] = __float_as_uint(r[2 * e]) ^ __float_as_uint(r[2 * e + 1]);
+            } else if (C::kSepP) {   // S already released: no reload possible, vote-first tiers
+              if (nvalid >= 32) sigmoid_row32<false, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+              else sigmoid_row32<true, kBf16>(r, pk, a2, b2, row_valid, nvalid);
+            } else {
+              if (nvalid >= 32) sigmoid_chunk32<false, kBf16, kT>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
+              else sigmoid_chunk32<true, kBf16, kT>(tmem + lane_addr + col, r, pk, a2, b2, row_valid, nvalid, spec);
+            }
+            if (C::kSepP) {
+              if (ch == 0) {   // PV_x(j-1) has read the previous P_x
+                sm100::mbar_wait(&pv_done[x], (xs & 1) ^ 1);
+                sm100::tc_fence_after();
+              }
+              sm100::tmem_st16(tmem + lane_addr + C::kColP + x * 64 + gp * 32 + ch * 16, pk);
+            } else {
+              sm100::tmem_st16(tmem + lane_addr + x * 128 + gp * 64 + ch * 16, pk);
+            }
           }
+          sm100::tmem_wait_st();
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&p_full[x]);
         }
-        sm100::tmem_wait_st();
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&p_full[x]);
-      }
+      };
+      if (spec4) key_loop(std::integral_constant<int, 4>{});
+      else key_loop(std::integral_constant<int, 2>{});
       // ---- epilogue: O_x rows, columns [gp D/2, +D/2) in 32-column pieces
+      if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 3584 + 3 * xo, 4092);
       sm100::mbar_wait(&o_full[x], xo & 1);
+      if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 3584 + 3 * xo + 1, 4092);
       sm100::tc_fence_after();
       const int qrow = qt * kTile + (int)row;
       const bool valid = qrow < nq;
@@ -373,6 +388,7 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
           }
         }
       }
+      if (lane == 0 && warp == 0) sm100::trace_event(args.trace, 3584 + 3 * xo + 2, 4092);
       ++xo;
     }
   }
@@ -382,8 +398,10 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                   kTile, lane, args.bshd, args.fill_pad, warp == C::kWarpFill ? 0 : 1, 2);
 
   if (kOutF32 && args.peer_o) sm100::fence_sys();   // this CTA's peer reductions before kernel completion
+  if (lane == 0) sm100::trace_event(args.trace, 4064 + (int)warp, 4092);   // per-warp end (trace builds)
   sm100::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) sm100::trace_globaltime(args.trace, 4095);
   if (warp == C::kWarpAlloc) sm100::tmem_dealloc<C::kTmemCols>(tmem);
 }
 
