@@ -22,10 +22,9 @@
 // which the warp scheduler favours):
 //   warps 0-15  compute: thread = key row (TMEM lane); all 16 warps process query half 0, then half 1;
 //               warpgroup w takes 16 queries [64q + 16w, +16) of half q
-//   warps 16-19 epilogue warpgroup: dS^T staging (TMEM -> swizzled smem operand of the dQ MMA), dQ_i
-//               drain (tcgen05.ld -> x alpha -> swizzled fp32 smem tile -> two TMA bulk tensor
-//               reduce-adds into the fp32 workspace, in L2), dK/dV of a finished key tile (x alpha
-//               for dK, round, store; padded rows = 0)
+//   warps 16-19 epilogue warpgroup: dQ_i drain (tcgen05.ld -> x alpha -> swizzled fp32 smem tile ->
+//               two TMA bulk tensor reduce-adds into the fp32 workspace, in L2), dK/dV of a finished
+//               key tile (x alpha for dK, round, store; padded rows = 0)
 //   warp 20     TMA: K_j, V_j (2 slots), Q_i + dO_i (2 stages)
 //   warp 21     MMA issuer (one elected thread); also tcgen05.cp of K_j, V_j into TMEM
 //   warp 22     TMEM allocator
@@ -50,15 +49,6 @@
 #endif
 #ifndef SIGATTN_BWD_SPEC_V2
 #define SIGATTN_BWD_SPEC_V2 1     // speculative tier 4 without the ordering barrier (sigmoid_chunk32 style)
-#endif
-#ifndef SIGATTN_BWD64_SPEC
-#define SIGATTN_BWD64_SPEC false  // ... in the d = 64 fused backward: vote first measured 1.5-8% faster
-#endif
-// 1: the compute warps store their packed dS^T straight into the swizzled smem operand of the dQ MMA
-// (beside the TMEM store): no TMEM read-back by the epilogue, no ds_copied hand-off in front of the
-// next tile's score MMAs.  0: the epilogue warpgroup stages dS^T from TMEM.
-#ifndef SIGATTN_BWD_DS_DIRECT
-#define SIGATTN_BWD_DS_DIRECT 1
 #endif
 namespace sigattn {
 
@@ -96,7 +86,7 @@ struct BwdCfg {
   static constexpr int kDSBytes = 2 * kTile * 128;
   static constexpr int kDQOff = kDSOff + 2 * kDSBytes;      // fp32 dQ staging tile for the TMA reduce-add
   static constexpr int kBarOff = kDQOff + kTile * D * 4;
-  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 2 + 1 + 1 + 2 + 2;
+  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kNumWG = 4;                           // compute warpgroups
   static constexpr int kWarpEpi = 4 * kNumWG, kWarpTMA = kWarpEpi + 4, kWarpMMA = kWarpTMA + 1,
@@ -155,7 +145,9 @@ struct TileIter {
 // vote; on a failed vote the scores are reloaded from s_taddr and the exact tiers run.  spec:
 // speculate tier 4 (updated to whether this chunk took tier 4, so a warp stops speculating while its
 // logits keep failing the vote).
-template <bool kMask, bool kSpec = true>
+// kTier: the speculated tier (4: <= -4, one FFMA2 per pair; 2: <= -2, three FMA-pipe ops), chosen per
+// work item from the bias as in the forward (kSpec4MaxBias).
+template <bool kMask, bool kSpec = true, int kTier = 4>
 __device__ __forceinline__ void bwd_sigma16(float (&v)[16], float a2, float b2, bool key_valid, int nvalid,
                                             uint32_t s_taddr, bool& spec) {
   if constexpr (!kSpec) {   // vote first (measured better for the d = 64 fused backward)
@@ -179,15 +171,18 @@ __device__ __forceinline__ void bwd_sigma16(float (&v)[16], float a2, float b2, 
         m = fmax3(m, v[e], v[e + 1]);
     }
 #pragma unroll
-    for (int e = 0; e < 16; e += 2) sigma2_fast4(v[e], v[e + 1], v[e], v[e + 1]);
-    if (__all_sync(0xffffffffu, !key_valid || m <= kFastT4)) return;
+    for (int e = 0; e < 16; e += 2) {
+      if constexpr (kTier == 4) sigma2_fast4(v[e], v[e + 1], v[e], v[e + 1]);
+      else sigma2_fast(v[e], v[e + 1], v[e], v[e + 1]);
+    }
+    if (__all_sync(0xffffffffu, !key_valid || m <= (kTier == 4 ? kFastT4 : kFastT))) return;
 #else
     if (sigma_row_spec4<16, kMask>(v, a2, b2, key_valid, nvalid)) return;   // v: scores in, P out
 #endif
     sm100::tmem_ld16(s_taddr, v);   // rare: some valid logit > -4
     sm100::tmem_wait_ld_dep16(v);
   }
-  spec = sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid) == 4;   // one inlined copy
+  spec = sigma_row<16, kMask, 0>(v, a2, b2, key_valid, nvalid) >= kTier;   // one inlined copy
 #else
   (void)s_taddr;
   (void)spec;
@@ -221,11 +216,11 @@ __device__ __forceinline__ void bwd_ds16(const float (&v)[16], const float (&dp)
 }
 
 // Both steps on 16 query columns of one key row (scores and dP^T already loaded).
-template <bool kMask, bool kBf16, bool kSum = false, bool kSpec = true>
+template <bool kMask, bool kBf16, bool kSum = false, bool kSpec = true, int kTier = 4>
 __device__ __forceinline__ void bwd_row16(float (&v)[16], const float (&dp)[16], uint32_t (&pp)[8], uint32_t (&dd)[8],
                                           float a2, float b2, bool key_valid, int nvalid, uint32_t s_taddr,
                                           bool& spec, float* dsum = nullptr) {
-  bwd_sigma16<kMask, kSpec>(v, a2, b2, key_valid, nvalid, s_taddr, spec);
+  bwd_sigma16<kMask, kSpec, kTier>(v, a2, b2, key_valid, nvalid, s_taddr, spec);
   bwd_ds16<kMask, kBf16, kSum>(v, dp, pp, dd, nvalid, dsum);
 }
 
@@ -260,8 +255,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* dq_empty = dq_full + 1;               // epilogue read dQ(t) out of TMEM
   uint64_t* acc_full = dq_empty + 1;
   uint64_t* acc_empty = acc_full + 1;
-  uint64_t* ds_copied = acc_empty + 1;            // [2] per query half: epilogue read dS^T from TMEM
-  uint64_t* ds_full = ds_copied + 2;              // [2] per dS smem buffer: both halves staged + fenced
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -275,8 +268,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&ds_free[i], 1);
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&p_full[i], kComputeWarps);       // every compute warp works on every half
-      sm100::mbar_init(&ds_copied[i], 4);
-      sm100::mbar_init(&ds_full[i], 4);                  // the 4 epilogue warps, after both halves
     }
     for (int i = 0; i < C::kQStages; ++i) {
       sm100::mbar_init(&qdo_full[i], 1);
@@ -418,8 +409,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const uint32_t b2 = tq & 1;
 #if !SIGATTN_DBG_MMAONLY
       sm100::mbar_wait(dq_empty, (tq & 1) ^ 1);                  // epilogue drained the accumulator
-      if (!SIGATTN_BWD_DS_DIRECT)   // (direct: p_full of both halves, waited above, covers the stores)
-        sm100::mbar_wait(&ds_full[b2], (tq >> 1) & 1);           // dS(tq) staged in smem, proxy-fenced
+      // dS(tq) in smem: p_full of both halves (waited by the caller) covers the compute warps' stores
 #endif
       if (lane == 0 && tq >= 40 && tq < 48) sm100::trace_event(args.trace, 3328 + (tq - 40) * 8 + 3, 4094);
       sm100::tc_fence_after();
@@ -463,7 +453,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
         MMA_TR(6);
 #if !SIGATTN_DBG_MMAONLY
-        if (kDQ && !SIGATTN_BWD_DS_DIRECT) sm100::mbar_wait(&ds_copied[0], t & 1);   // dS^T(t, q0) left TMEM before S/dP(t+1, q0) land there
 #endif
         MMA_TR(7);
         sm100::tc_fence_after();
@@ -491,7 +480,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       MMA_TR(1);
       if (nxt.valid) {
 #if !SIGATTN_DBG_MMAONLY
-        if (kDQ && !SIGATTN_BWD_DS_DIRECT) sm100::mbar_wait(&ds_copied[1], t & 1);
 #endif
         sm100::tc_fence_after();
         if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 1);
@@ -513,7 +501,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t row = quarter * 32 + lane;          // key row within the tile = TMEM lane
     const uint32_t lane_addr = (quarter * 32) << 16;
     const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
-    (void)ds_row;
     uint32_t t = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
@@ -528,6 +515,8 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       float db_acc = 0.f;
       bool spec = true;   // speculate tier 4 while the last chunk took it
+      // vote first (measured 1.5% faster than speculating the <= -4 tier on C3, and 2-3% faster than
+      // speculating the <= -2 tier for b > kSpec4MaxBias at N = 1-2K)
       for (int i = 0; i < nqt; ++i, ++t) {
 #pragma unroll
         for (int qh = 0; qh < 2; ++qh) {
@@ -552,14 +541,14 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           // rows of padded keys)
           const int ncol = nq - (sweep_tile(kt, i, nqt) * kTile + qh * 64 + (int)w4 * 16);
           uint32_t pp[8], dd[8];
-          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB, SIGATTN_BWD64_SPEC>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
-          else bwd_row16<true, kBf16, kDB, SIGATTN_BWD64_SPEC>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
+          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB, false>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
+          else bwd_row16<true, kBf16, kDB, false>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
           BWD_TR(qh == 0 ? 1 : 4);
           // P^T / dS^T over the first half of this warp's own (already read) columns; the epilogue
           // warpgroup stages dS^T into shared memory for the dQ MMA
           sm100::tmem_st8(tmem + lane_addr + s_col, pp);
           sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
-          if (kDQ && SIGATTN_BWD_DS_DIRECT) {
+          if constexpr (kDQ) {
             // queries [64 qh + 16 w4, +16) of key row `row` = 16-byte chunks 2 w4, 2 w4 + 1 of the
             // half's 128-byte row, SW128 swizzle (chunk c at slot c ^ (row & 7))
             if (qh == 0) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) MMA done with the buffer
@@ -579,20 +568,17 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       if constexpr (kDB) dbias_flush(args.dbias, b, db_acc, lane);
     }
   } else if (warp < C::kWarpTMA && !SIGATTN_DBG_MMAONLY && warp >= kComputeWarps) {
-    // ===================== epilogue warpgroup: dS^T staging, dQ drain, dK/dV =====================
-    // Per query tile t: for each half, copy the packed dS^T the compute warps left in TMEM into the
-    // swizzled smem operand of the dQ MMA (so the compute warps never wait on shared-memory stores or
-    // proxy fences), then drain dQ(t-1) -- one tile behind, so the drain never delays the copies the
-    // MMA warp is waiting for.
+    // ===================== epilogue warpgroup: dQ drain, dK/dV =====================
+    // The compute warps store dS^T into the dQ MMA's shared-memory operand themselves (beside the TMEM
+    // copy the dK MMA reads), so the tile's score MMAs never wait on a TMEM read-back; this warpgroup
+    // drains dQ(t) as soon as it lands and writes dK/dV when a key tile is finished.
     const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;
     const uint32_t lane_addr = (quarter * 32) << 16;
-    const uint32_t ds_row = sm100::smem_u32(smem + C::kDSOff + (row >> 3) * 1024 + (row & 7) * 128);
     const float alpha = args.scale;
     // dQ(tq) += alpha * TMEM dQ through the TMA: the fp32 tile is written (SW128, two 32-column
     // boxes) into a dedicated staging buffer, then one thread issues two bulk tensor reduce-adds
-    // into the fp32 accumulator (the adds happen in L2; no per-lane atomics).  (Reusing the dS
-    // buffer instead put the reduce's smem read on the dS staging path: +2000 clk per tile.)
+    // into the fp32 accumulator (the adds happen in L2; no per-lane atomics).
     constexpr uint32_t kEpiThread0 = 32 * kComputeWarps;
 #define EPI_TR(tt, e) if (threadIdx.x == kEpiThread0 && (tt) >= 40 && (tt) < 48) sm100::trace_event(args.trace, 3072 + ((tt) - 40) * 16 + (e), 4094)
     auto drain_dq = [&](uint32_t tq, int zh, int i) {
@@ -641,8 +627,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       EPI_TR(tq + 1, 10);
     };
     uint32_t t = 0, item_c = 0;
-    bool pend = false;            // a dQ tile waiting to be drained
-    int pend_zh = 0, pend_i = 0;
     for (int it = first_item(); it < n_items; it = next_item(it)) {
       const int4 item = args.items[it];
       const int b = item.x, h = item.y, kt = item.z, nqt = item.w;
@@ -651,44 +635,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       const int nk = clampi(args.seqlens_k ? args.seqlens_k[b] : args.Nk, 0, args.Nk);
       const size_t zh = (size_t)(b * args.H + h);
       for (int i = 0; i < nqt * kDQ; ++i, ++t) {
-        if (SIGATTN_BWD_DS_DIRECT) {   // no staging: drain dQ(t) as soon as it lands
-          drain_dq(t, (int)zh, sweep_tile(kt, i, nqt));
-          continue;
-        }
-        const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
-#pragma unroll 1
-        for (int qh = 0; qh < 2; ++qh) {
-          sm100::mbar_wait(&p_full[qh], t & 1);
-          EPI_TR(t, qh == 0 ? 0 : 4);
-          sm100::tc_fence_after();
-          uint32_t d[4][8];   // packed dS^T of queries [64 qh + 16 g, +16) at columns 64 qh + 16 g + [0, 8)
-#pragma unroll
-          for (int g = 0; g < 4 * !SIGATTN_DBG_EPI_NOLD; ++g)
-            sm100::tmem_ld8(tmem + lane_addr + C::kColDP + qh * 64 + g * 16, d[g]);
-          sm100::tmem_wait_ld_dep4x8(d);
-          sm100::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&ds_copied[qh]);
-          EPI_TR(t, qh == 0 ? 1 : 5);
-          if (qh == 0) {
-            sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);   // dQ(t-2) MMA done with the buffer
-            EPI_TR(t, 2);
-          }
-#pragma unroll
-          for (int c = 0; c < 8 * !SIGATTN_DBG_NOSTAGE; ++c)   // 16-byte chunk c = queries [8c, 8c + 8) of this half, SW128 swizzle
-            sm100::st_shared_v4(dsr + qh * (kTile * 128) + ((c ^ (row & 7)) * 16), d[c >> 1][(c & 1) * 4],
-                                d[c >> 1][(c & 1) * 4 + 1], d[c >> 1][(c & 1) * 4 + 2], d[c >> 1][(c & 1) * 4 + 3]);
-          if (qh == 1) {   // one proxy fence covers both halves' stores
-            sm100::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(&ds_full[t & 1]);
-          }
-          EPI_TR(t, qh == 0 ? 3 : 6);
-        }
-        if (pend) drain_dq(t - 1, pend_zh, pend_i);
-        pend = true;
-        pend_zh = (int)zh;
-        pend_i = sweep_tile(kt, i, nqt);
+        drain_dq(t, (int)zh, sweep_tile(kt, i, nqt));   // dQ(t) as soon as it lands
       }
       // ---- dV, dK rows of this key tile (dK scaled by alpha)
       sm100::mbar_wait_backoff(acc_full, item_c & 1);
@@ -734,7 +681,6 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
       ++item_c;
     }
-    if (kDQ && pend) drain_dq(t - 1, pend_zh, pend_i);
     if (kDQ && threadIdx.x == kEpiThread0) sm100::bulk_wait_group<0>();   // reduce-adds complete before exit
   }
 

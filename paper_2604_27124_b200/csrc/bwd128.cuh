@@ -18,6 +18,7 @@
 // TMEM: S^T [0,64) dP^T [64,128) dV [128,256) dK [256,384) dQ^T [384,448).
 // Shared memory: K, V (single slot, 2 x 32 KB), Q_i + dO_i ring (3 x 2 x 16 KB), dS^T (2 x 16 KB).
 #pragma once
+#include <type_traits>
 #include "bwd.cuh"
 
 namespace sigattn {
@@ -262,43 +263,49 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
       const bool key_valid = kt * kTile + (int)row < nk;
       const bool warp_keys_valid = __all_sync(0xffffffffu, key_valid);
       float db_acc = 0.f;
-      bool spec = true;   // speculate tier 4 while the last chunk took it
-      for (int i = 0; i < nqt; ++i, ++t) {
-        SIGATTN_COMPUTE_WAIT(s_full, t & 1);
-        if (kDQ) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
-        sm100::tc_fence_after();
-        float s[16], dp[16];
-        sm100::tmem_ld16(tmem + lane_addr + s_col, s);
-        sm100::tmem_wait_ld_dep16(s);
-        const int ncol = nq - (i * C::kQT + (int)w4 * 16);
-        const bool full = warp_keys_valid && ncol >= 16;
-        const int nv = full ? 16 : (key_valid ? ncol : 0);
-        if (full) bwd_sigma16<false>(s, a2, b2, true, 16, tmem + lane_addr + s_col, spec);
-        else bwd_sigma16<true>(s, a2, b2, key_valid, nv, tmem + lane_addr + s_col, spec);
-        // dP^T lands after S^T: sigma above overlaps the dP^T MMAs
-        SIGATTN_COMPUTE_WAIT(dp_full, t & 1);
-        sm100::tc_fence_after();
-        sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
-        sm100::tmem_wait_ld_dep16(dp);
-        uint32_t pp[8], dd[8];
-        if (full) bwd_ds16<false, kBf16, kDB>(s, dp, pp, dd, 16, &db_acc);
-        else bwd_ds16<true, kBf16, kDB>(s, dp, pp, dd, nv, &db_acc);
-        sm100::tmem_st8(tmem + lane_addr + s_col, pp);
-        sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
-        if constexpr (kDQ) {
-          const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
+      bool spec = true;   // speculate while the last chunk took the speculated tier
+      // the query loop, instantiated for the item's speculative sigma tier (one hot copy per item)
+      auto query_loop = [&](auto tier_c) {
+        constexpr int kT = decltype(tier_c)::value;
+        for (int i = 0; i < nqt; ++i, ++t) {
+          SIGATTN_COMPUTE_WAIT(s_full, t & 1);
+          if (kDQ) sm100::mbar_wait(&ds_free[t & 1], ((t >> 1) & 1) ^ 1);
+          sm100::tc_fence_after();
+          float s[16], dp[16];
+          sm100::tmem_ld16(tmem + lane_addr + s_col, s);
+          sm100::tmem_wait_ld_dep16(s);
+          const int ncol = nq - (i * C::kQT + (int)w4 * 16);
+          const bool full = warp_keys_valid && ncol >= 16;
+          const int nv = full ? 16 : (key_valid ? ncol : 0);
+          if (full) bwd_sigma16<false, true, kT>(s, a2, b2, true, 16, tmem + lane_addr + s_col, spec);
+          else bwd_sigma16<true, true, kT>(s, a2, b2, key_valid, nv, tmem + lane_addr + s_col, spec);
+          // dP^T lands after S^T: sigma above overlaps the dP^T MMAs
+          SIGATTN_COMPUTE_WAIT(dp_full, t & 1);
+          sm100::tc_fence_after();
+          sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
+          sm100::tmem_wait_ld_dep16(dp);
+          uint32_t pp[8], dd[8];
+          if (full) bwd_ds16<false, kBf16, kDB>(s, dp, pp, dd, 16, &db_acc);
+          else bwd_ds16<true, kBf16, kDB>(s, dp, pp, dd, nv, &db_acc);
+          sm100::tmem_st8(tmem + lane_addr + s_col, pp);
+          sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
+          if constexpr (kDQ) {
+            const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes;
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const uint32_t chunk = (uint32_t)(w4 * 2 + u) ^ (row & 7);
-            sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+            for (int u = 0; u < 2; ++u) {
+              const uint32_t chunk = (uint32_t)(w4 * 2 + u) ^ (row & 7);
+              sm100::st_shared_v4(dsr + chunk * 16, dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+            }
           }
+          sm100::tmem_wait_st();
+          if (kDQ) sm100::fence_proxy_async_smem();
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(p_full);
         }
-        sm100::tmem_wait_st();
-        if (kDQ) sm100::fence_proxy_async_smem();
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(p_full);
-      }
+      };
+      if (bias <= kSpec4MaxBias) query_loop(std::integral_constant<int, 4>{});
+      else query_loop(std::integral_constant<int, 2>{});
       if constexpr (kDB) dbias_flush(args.dbias, b, db_acc, lane);
     }
   } else if (warp < C::kWarpTMA) {
