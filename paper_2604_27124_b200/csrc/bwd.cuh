@@ -86,7 +86,7 @@ struct BwdCfg {
   static constexpr int kDSBytes = 2 * kTile * 128;
   static constexpr int kDQOff = kDSOff + 2 * kDSBytes;      // fp32 dQ staging tile for the TMA reduce-add
   static constexpr int kBarOff = kDQOff + kTile * D * 4;
-  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1;
+  static constexpr int kNumBars = 2 + 2 + 2 * kQStages + 2 + 2 + 2 + 1 + 1 + 1 + 1 + 2;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
   static constexpr int kNumWG = 4;                           // compute warpgroups
   static constexpr int kWarpEpi = 4 * kNumWG, kWarpTMA = kWarpEpi + 4, kWarpMMA = kWarpTMA + 1,
@@ -255,6 +255,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint64_t* dq_empty = dq_full + 1;               // epilogue read dQ(t) out of TMEM
   uint64_t* acc_full = dq_empty + 1;
   uint64_t* acc_empty = acc_full + 1;
+  uint64_t* dp_full = acc_empty + 1;              // [2] per query half: dP^T in TMEM (S^T: s_full)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const uint32_t warp = sm100::warp_id();
@@ -267,6 +268,7 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::mbar_init(&kv_empty[i], 1);
       sm100::mbar_init(&ds_free[i], 1);
       sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&dp_full[i], 1);
       sm100::mbar_init(&p_full[i], kComputeWarps);       // every compute warp works on every half
     }
     for (int i = 0; i < C::kQStages; ++i) {
@@ -348,23 +350,27 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         sm100::tmem_cp_128x256b(tmem + C::kColV + kk * 8, sm100::sdesc_add(sm100::make_sdesc_sw128(va, 16, 1024), kk * 32));
       }
     };
-    // S^T_q = K Q_q^T and dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; A from TMEM)
-    auto mma1 = [&](uint32_t kvb, uint32_t st, uint32_t q) {
-      const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
-      (void)kvb;
+    // S^T_q = K Q_q^T, then dP^T_q = V dO_q^T  (M = 128 keys, N = 64 queries, K = d; A from TMEM),
+    // each signalled on its own barrier: sigma needs only S^T
+    auto mma_s = [&](uint32_t st, uint32_t q) {
+      const uint32_t qa = q_base + st * C::kTileBytes + q * 8192;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
         sm100::mma_ts(tmem + C::kColS + q * 64, tmem + C::kColK + kk * 8,
                       sm100::sdesc_add(sm100::make_sdesc_sw128(qa, 16, 1024), kk * 32), idesc_s, kk > 0);
+      sm100::mma_commit(&s_full[q]);
+    };
+    auto mma_dp = [&](uint32_t st, uint32_t q) {
+      const uint32_t da = do_base + st * C::kTileBytes + q * 8192;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
         sm100::mma_ts(tmem + C::kColDP + q * 64, tmem + C::kColV + kk * 8,
                       sm100::sdesc_add(sm100::make_sdesc_sw128(da, 16, 1024), kk * 32), idesc_s, kk > 0);
-      sm100::mma_commit(&s_full[q]);
+      sm100::mma_commit(&dp_full[q]);
     };
     // dV += P^T_q dO_q ; dK += dS^T_q Q_q   (M = keys, N = d, K = 64 queries; A from TMEM)
-    auto mma2 = [&](uint32_t st, uint32_t q, bool first) {
-      const uint32_t qa = q_base + st * C::kTileBytes + q * 8192, da = do_base + st * C::kTileBytes + q * 8192;
+    auto mma_dv = [&](uint32_t st, uint32_t q, bool first) {
+      const uint32_t da = do_base + st * C::kTileBytes + q * 8192;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         // queries [64q + 16kk, +16): warpgroup kk packed them at S cols 64q + 16kk + [0, 8)
@@ -373,6 +379,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                       sm100::sdesc_add(sm100::make_sdesc_sw128(da, kTile * 128, 1024), kk * 2048), idesc_acc,
                       (first && kk == 0) ? 0u : 1u);
       }
+    };
+    auto mma_dk = [&](uint32_t st, uint32_t q, bool first) {
+      const uint32_t qa = q_base + st * C::kTileBytes + q * 8192;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const uint32_t a_col = q * 64 + kk * 16;
@@ -390,8 +399,10 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       sm100::tc_fence_after();
       if (sm100::elect_one()) {
         copy_kv(cur.item_c & 1);
-        mma1(cur.item_c & 1, 0, 0);
-        mma1(cur.item_c & 1, 0, 1);
+        mma_s(0, 0);
+        mma_dp(0, 0);
+        mma_s(0, 1);
+        mma_dp(0, 1);
       }
       __syncwarp();
     }
@@ -443,8 +454,12 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #if !SIGATTN_DBG_MMAONLY
       if (cur.i == 0) sm100::mbar_wait(acc_empty, (cur.item_c & 1) ^ 1);   // epilogue read previous dV/dK
 #endif
+      // Per half q: dV(t, q) | S(t+1, q) | dK(t, q) | dP(t+1, q).  S(t+1, q) overwrites the S^T columns
+      // holding P^T(t, q) right after dV(t, q) has read them, and dP(t+1, q) the dP^T columns holding
+      // dS^T(t, q) after dK(t, q) (tcgen05 ops of one thread execute in order), so the compute warps
+      // get S(t+1, q) eight MMAs after P(t, q) instead of sixteen, and start sigma before dP lands.
       sm100::tc_fence_after();
-      if (sm100::elect_one()) mma2(st, 0, cur.i == 0);
+      if (sm100::elect_one()) mma_dv(st, 0, cur.i == 0);
       __syncwarp();
       MMA_TR(0);
       if (nxt.valid) {
@@ -452,18 +467,21 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         MMA_TR(5);
         sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
         MMA_TR(6);
-#if !SIGATTN_DBG_MMAONLY
-#endif
-        MMA_TR(7);
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
           // the copy executes after every earlier MMA (tcgen05 ops of one thread run in order), so
-          // S/dP(i, q1) has finished reading the previous K/V columns
+          // S/dP(t, q1) have finished reading the previous K/V columns
           if (nxt.i == 0) copy_kv(nxt.item_c & 1);
-          mma1(nxt.item_c & 1, st1, 0);
+          mma_s(st1, 0);
         }
         __syncwarp();
       }
+      MMA_TR(7);
+      if (sm100::elect_one()) {
+        mma_dk(st, 0, cur.i == 0);
+        if (nxt.valid) mma_dp(st1, 0);
+      }
+      __syncwarp();
       if (lane == 0) sm100::trace_event(args.trace, 1 * 512 + t, 1 * 512 + 512);
 #if !SIGATTN_DBG_MMAONLY
       MMA_WAIT_P(&p_full[1], t & 1);
@@ -471,20 +489,16 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       if (lane == 0) sm100::trace_event(args.trace, 2 * 512 + t, 2 * 512 + 512);
       sm100::tc_fence_after();
       if (sm100::elect_one()) {
-        mma2(st, 1, false);
+        mma_dv(st, 1, false);
+        if (nxt.valid) mma_s(st1, 1);
+        mma_dk(st, 1, false);
         sm100::mma_commit(&qdo_empty[st]);                       // last readers of Q_i, dO_i
         if (cur.i == cur.nqt - 1) sm100::mma_commit(acc_full);   // dV, dK of this key tile are final
         if (cur.i == 0 && args.counters) atomicAdd(args.counters + 1, (unsigned long long)cur.nqt);
+        if (nxt.valid) mma_dp(st1, 1);
       }
       __syncwarp();
       MMA_TR(1);
-      if (nxt.valid) {
-#if !SIGATTN_DBG_MMAONLY
-#endif
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) mma1(nxt.item_c & 1, st1, 1);
-        __syncwarp();
-      }
       MMA_TR(2);
       prev_kvb = kvb;
       prev_last = cur.i == cur.nqt - 1;
@@ -534,18 +548,25 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #endif
           float s[16], dp[16];
           sm100::tmem_ld16(tmem + lane_addr + s_col, s);
-          sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
           sm100::tmem_wait_ld_dep16(s);
-          sm100::tmem_wait_ld_dep16(dp);
           // valid query columns here; the masked variant is chosen warp-uniformly (it also zeroes the
           // rows of padded keys)
           const int ncol = nq - (sweep_tile(kt, i, nqt) * kTile + qh * 64 + (int)w4 * 16);
+          const bool full = warp_keys_valid && ncol >= 16;
+          const int nv = full ? 16 : (key_valid ? ncol : 0);
+          if (full) bwd_sigma16<false, false>(s, a2, b2, true, 16, tmem + lane_addr + s_col, spec);
+          else bwd_sigma16<true, false>(s, a2, b2, key_valid, nv, tmem + lane_addr + s_col, spec);
+          // dP^T(t, q) lands after S^T(t, q): sigma above overlaps the dP^T MMAs
+          SIGATTN_COMPUTE_WAIT(&dp_full[qh], t & 1);
+          sm100::tc_fence_after();
+          sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
+          sm100::tmem_wait_ld_dep16(dp);
           uint32_t pp[8], dd[8];
-          if (warp_keys_valid && ncol >= 16) bwd_row16<false, kBf16, kDB, false>(s, dp, pp, dd, a2, b2, true, 16, tmem + lane_addr + s_col, spec, &db_acc);
-          else bwd_row16<true, kBf16, kDB, false>(s, dp, pp, dd, a2, b2, key_valid, key_valid ? ncol : 0, tmem + lane_addr + s_col, spec, &db_acc);
+          if (full) bwd_ds16<false, kBf16, kDB>(s, dp, pp, dd, 16, &db_acc);
+          else bwd_ds16<true, kBf16, kDB>(s, dp, pp, dd, nv, &db_acc);
           BWD_TR(qh == 0 ? 1 : 4);
-          // P^T / dS^T over the first half of this warp's own (already read) columns; the epilogue
-          // warpgroup stages dS^T into shared memory for the dQ MMA
+          // P^T / dS^T over the first half of this warp's own (already read) columns, and dS^T into
+          // the dQ MMA's shared-memory operand
           sm100::tmem_st8(tmem + lane_addr + s_col, pp);
           sm100::tmem_st8(tmem + lane_addr + dp_col, dd);
           if constexpr (kDQ) {

@@ -731,3 +731,38 @@ def test_output_buffer_validation():
         sa.sigattn_fwd(q, k, v, workspace=torch.empty(16, dtype=torch.uint8, device="cuda"))
     with pytest.raises(ValueError, match="workspace too small"):
         sa.sigattn_bwd(q, k, v, do, workspace=torch.empty(16, dtype=torch.uint8, device="cuda"))
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("layout", ["bhsd", "bshd"])
+def test_pad_fill_many_slabs(d, layout):
+    """The idle-warp pad fills (a 32-slab step per lane group, 512-byte blocks dealt over all workers)
+    at B*H = 144 slabs -- five steps, the last one partial -- with empty, one-row, tile-edge and full
+    sequences and n_q != n_k: outputs prefilled with NaN, every padded row exactly 0 (P:593, P:638,
+    P:692), valid rows equal to the oracle; the [B, N, H, d] layout bitwise equal to [B, H, N, d]."""
+    sa = _sa()
+    lq = [0, 1, 127, 128, 129, 255, 384, 300] * 3
+    lk = [384, 5, 0, 128, 200, 129, 384, 1] * 3
+    cfg = I.Config("fill", B=24, H=6, N=384, d=d, lengths=lq, Nk=384, lengths_k=lk, seed=70 + d)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    alpha, b = 1.0 / math.sqrt(d), -math.log(384)
+    nan = lambda t: torch.full_like(t, float("nan"))  # noqa: E731
+    if layout == "bhsd":
+        o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b, out=nan(q))
+        dq, dk, dv = sa.sigattn_bwd(q, k, v, do, nq, nk, alpha, b, dq=nan(q), dk=nan(k), dv=nan(v))
+    else:
+        qs, ks, vs, dos = (_to_bshd(t) for t in (q, k, v, do))
+        o = sa.sigattn_fwd(qs, ks, vs, nq, nk, alpha, b, out=nan(qs), layout="bshd").transpose(1, 2)
+        dq, dk, dv = (t.transpose(1, 2) for t in sa.sigattn_bwd(qs, ks, vs, dos, nq, nk, alpha, b, dq=nan(qs),
+                                                                  dk=nan(ks), dv=nan(vs), layout="bshd"))
+    torch.cuda.synchronize()
+    bias = np.full(cfg.B, b)
+    ro = oracle.fwd(f64(q), f64(k), f64(v), cfg.nq, cfg.nk, alpha, bias)
+    rdq, rdk, rdv = oracle.bwd(f64(q), f64(k), f64(v), f64(do), cfg.nq, cfg.nk, alpha, bias)
+    for name, got, ref, lens in (("o", o, ro, lq), ("dq", dq, rdq, lq), ("dk", dk, rdk, lk), ("dv", dv, rdv, lk)):
+        g = f64(got)
+        assert np.isfinite(g).all(), f"{name}: an element was never written"
+        e = relerr(g, ref)
+        assert e <= BF16_TOL, f"{name} rel err {e}"
+        for bb, n in enumerate(lens):
+            assert (g[bb, :, n:] == 0).all(), f"{name}: padded rows of sequence {bb} not exactly 0"
