@@ -428,24 +428,34 @@ def main_ours(args):
     ms_step = ms_total / K
     value = wl.total_flops / (ms_step * 1e-3) / 1e12
 
-    # ---- end to end through the public API with host (pinned) buffers (C3 only)
+    # ---- end to end through the public API with host (pinned) buffers: every step copies the step's
+    # inputs host -> device and reads O, dQ, dK, dV back.  Padding-aware transfers
+    # (sa.copy_valid_rows, sigattn_copy_valid_rows): only the valid rows of each (b, h) slab cross
+    # PCIe; the persistent device buffers' padded rows stay zero (zeroed once), and the host output
+    # buffers' padded rows are zeroed once -- the padded output rows are exact zeros by contract.
     e2e = None
     if not args.no_e2e:
         alpha, bias = wl.alpha, wl.bias
         hq, hk, hv, hdo = (t_.cpu().pin_memory() for t_ in (wl.q, wl.k, wl.v, wl.do))
         hnq, hnk = wl.nq.cpu().pin_memory(), wl.nk.cpu().pin_memory()
-        ho, hdq, hdk, hdv = (torch.empty(t_.shape, dtype=t_.dtype, pin_memory=True) for t_ in (wl.q, wl.q, wl.k, wl.v))
+        lq, lk = hnq.tolist(), hnk.tolist()
+        ho, hdq, hdk, hdv = (torch.zeros(t_.shape, dtype=t_.dtype).pin_memory() for t_ in (wl.q, wl.q, wl.k, wl.v))
+        dq_, dk_, dv_, ddo = (torch.zeros_like(t_) for t_ in (wl.q, wl.k, wl.v, wl.do))
+        oo, g1, g2, g3 = (torch.empty_like(t_) for t_ in (wl.q, wl.q, wl.k, wl.v))
+        snq, snk = torch.empty_like(wl.nq), torch.empty_like(wl.nk)
+        moved = [0, 0]
 
         def e2e_step():
-            dq_, dk_, dv_ = (t_.to(dev, non_blocking=True) for t_ in (hq, hk, hv))
-            ddo = hdo.to(dev, non_blocking=True)
-            snq, snk = hnq.to(dev, non_blocking=True), hnk.to(dev, non_blocking=True)
-            oo = sa.sigattn_fwd(dq_, dk_, dv_, snq, snk, alpha, bias, workspace=wl.fws)
-            g1, g2, g3 = sa.sigattn_bwd(dq_, dk_, dv_, ddo, snq, snk, alpha, bias, workspace=wl.ws)
-            ho.copy_(oo, non_blocking=True)
-            hdq.copy_(g1, non_blocking=True)
-            hdk.copy_(g2, non_blocking=True)
-            hdv.copy_(g3, non_blocking=True)
+            h2d = sum(sa.copy_valid_rows(h_, d_, lens) for h_, d_, lens in
+                      ((hq, dq_, lq), (hk, dk_, lk), (hv, dv_, lk), (hdo, ddo, lq)))
+            snq.copy_(hnq, non_blocking=True)
+            snk.copy_(hnk, non_blocking=True)
+            sa.sigattn_fwd(dq_, dk_, dv_, snq, snk, alpha, bias, out=oo, workspace=wl.fws)
+            sa.sigattn_bwd(dq_, dk_, dv_, ddo, snq, snk, alpha, bias, dq=g1, dk=g2, dv=g3, workspace=wl.ws)
+            d2h = sum(sa.copy_valid_rows(d_, h_, lens) for d_, h_, lens in
+                      ((oo, ho, lq), (g1, hdq, lq), (g2, hdk, lk), (g3, hdv, lk)))
+            moved[0] = h2d + hnq.numel() * hnq.element_size() + hnk.numel() * hnk.element_size()
+            moved[1] = d2h
 
         e2e_step()
         torch.cuda.synchronize()
@@ -460,12 +470,11 @@ def main_ours(args):
         e_ms = torch.tensor([s2.elapsed_time(t2) / args.e2e_steps], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        h2d = sum(t_.numel() * t_.element_size() for t_ in (hq, hk, hv, hdo, hnq, hnk))
-        d2h = sum(t_.numel() * t_.element_size() for t_ in (ho, hdq, hdk, hdv))
         e2e = {"value": wl.total_flops / (float(e_ms.item()) * 1e-3) / 1e12, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": int(moved[0]), "d2h_bytes_per_step": int(moved[1]),
                "ms_per_step": float(e_ms.item()), "steps": args.e2e_steps,
-               "path": "pinned host -> sigattn_fwd/sigattn_bwd (public API) -> pinned host, O and dQ/dK/dV read back"}
+               "path": "pinned host -> copy_valid_rows (valid rows of Q, K, V, dO) -> sigattn_fwd/sigattn_bwd "
+                       "(public API) -> copy_valid_rows -> pinned host (O, dQ, dK, dV); padded rows never cross PCIe"}
 
     peak, peak_sus, peak_src = load_peaks()
     bwd_tflops = wl.rank_bwd_flops / (bwd_ms * 1e-3) / 1e12

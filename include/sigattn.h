@@ -159,6 +159,21 @@ sigattn_status sigattn_mask_to_index(const uint8_t* key_padding_mask, int B, int
 sigattn_status sigattn_permute_rows(const void* src, void* dst, const int32_t* index, int B, int H, int N,
                                     int d, int scatter, void* stream);
 
+/* Padding-aware host <-> device transfer (the end-to-end path of a padded batch): copies only the
+ * VALID rows [0, lens[b]) of every (b, h) slab of a 16- or 32-bit [B, H, N, d] tensor (layout_bshd:
+ * [B, N, H, d], whose valid rows of sequence b are one contiguous block) from src to dst, as
+ * cudaMemcpy2DAsync / cudaMemcpyAsync on `stream` -- one call per sequence; rows past lens[b] of dst
+ * are not touched.  The kernels never read padded input rows beyond the last valid 128-row tile
+ * and write padded output rows as zeros, so a caller that keeps persistent
+ * buffers whose padded rows are zero (or passes SIGATTN_F_SANITIZE_PAD) moves only the valid
+ * bytes across PCIe.  host_lens: HOST int32 [B], clamped to [0, N].  kind: 1 host -> device,
+ * 2 device -> host, 3 device -> device (cudaMemcpyKind values).  row_bytes = d * element size, a
+ * multiple of 16.  Returns the bytes copied through *bytes_out when it is non-NULL.  Argument
+ * errors return SIGATTN_EINVAL before any copy is enqueued.                                       */
+sigattn_status sigattn_copy_valid_rows(const void* src, void* dst, int B, int H, int N, int row_bytes,
+                                       const int32_t* host_lens, int layout_bshd, int kind, void* stream,
+                                       int64_t* bytes_out);
+
 /* Instrumentation (bench / tests).  sigattn_launch_count(): number of kernels this library has
  * launched in this process so far (all entry points).  sigattn_set_profile_events(): thread-local;
  * when an event pair is non-NULL, the next sigattn_fwd / sigattn_bwd calls on this thread record

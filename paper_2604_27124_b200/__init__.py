@@ -5,7 +5,8 @@ This package is the thin Python boundary (argument marshalling) plus the multi-G
 """
 from .attention import (sigattn_bwd, sigattn_fwd, sigattn_mask_to_seqlens, sigmoid_attention,  # noqa: F401
                         valid_flops, worklist_host, bwd_workspace_bytes, fwd_workspace_bytes, resolve_bias, sigattn_mask_to_index,
-                        sigattn_permute_rows)
+                        sigattn_permute_rows, copy_valid_rows)
 
 __all__ = ["sigattn_fwd", "sigattn_bwd", "sigattn_mask_to_seqlens", "sigmoid_attention", "valid_flops",
-           "worklist_host", "bwd_workspace_bytes", "fwd_workspace_bytes", "resolve_bias", "sigattn_mask_to_index", "sigattn_permute_rows"]
+           "worklist_host", "bwd_workspace_bytes", "fwd_workspace_bytes", "resolve_bias", "sigattn_mask_to_index", "sigattn_permute_rows",
+           "copy_valid_rows"]

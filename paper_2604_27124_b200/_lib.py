@@ -29,7 +29,8 @@ EXPORTED = ["sigattn_fwd", "sigattn_fwd_workspace_bytes", "sigattn_bwd", "sigatt
             "sigattn_launch_count", "sigattn_set_profile_events", "sigattn_set_trace_buffer",
             "sigattn_set_debug_counters", "sigattn_mask_to_index", "sigattn_permute_rows",
             "sigattn_fwd_cp", "sigattn_bwd_cp", "sigattn_bwd_cp_workspace_bytes", "sigattn_cp_finalize",
-            "sigattn_ipc_handle_bytes", "sigattn_ipc_export", "sigattn_ipc_import", "sigattn_ipc_close"]
+            "sigattn_ipc_handle_bytes", "sigattn_ipc_export", "sigattn_ipc_import", "sigattn_ipc_close",
+            "sigattn_copy_valid_rows"]
 
 
 class SigattnParams(ctypes.Structure):
@@ -100,6 +101,10 @@ def load():
         lib.sigattn_permute_rows.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, vp]
         lib.sigattn_permute_rows.restype = ctypes.c_int
+    if hasattr(lib, "sigattn_copy_valid_rows"):
+        lib.sigattn_copy_valid_rows.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
+                                                ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int64)]
+        lib.sigattn_copy_valid_rows.restype = ctypes.c_int
     if hasattr(lib, "sigattn_fwd_cp"):
         CP = ctypes.POINTER(SigattnCpParams)
         lib.sigattn_fwd_cp.argtypes = [P, CP, vp, vp, vp, vp, ctypes.c_size_t, vp]

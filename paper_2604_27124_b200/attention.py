@@ -252,6 +252,33 @@ def sigattn_mask_to_index(key_padding_mask: torch.Tensor):
     return index, seqlens
 
 
+def copy_valid_rows(src: torch.Tensor, dst: torch.Tensor, lens, layout: str = "bhsd") -> int:
+    """Padding-aware transfer: copy only rows [0, lens[b]) of every (b, h) slab of src into dst (host
+    <-> device or device <-> device, asynchronous on the current stream of the CUDA side); rows past
+    lens[b] of dst are left as they are.  lens: host sequence of B ints (a CPU tensor or list).
+    Returns the bytes copied.  See include/sigattn.h sigattn_copy_valid_rows."""
+    lib = _lib.load()
+    if src.shape != dst.shape or src.dtype != dst.dtype or not src.is_contiguous() or not dst.is_contiguous():
+        raise ValueError("sigattn: copy_valid_rows needs contiguous tensors of one shape and dtype")
+    if src.is_cuda == dst.is_cuda and not src.is_cuda:
+        raise ValueError("sigattn: copy_valid_rows copies to or from a CUDA tensor")
+    if src.dim() != 4:
+        raise ValueError("sigattn: copy_valid_rows needs a [B, H, N, d] (or [B, N, H, d]) tensor")
+    B = src.shape[0]
+    H, N = (src.shape[2], src.shape[1]) if layout == "bshd" else (src.shape[1], src.shape[2])
+    lens_h = torch.as_tensor(lens, dtype=torch.int32).cpu().contiguous()
+    if lens_h.numel() != B:
+        raise ValueError("sigattn: lens must have B entries")
+    kind = 1 if dst.is_cuda and not src.is_cuda else 2 if src.is_cuda and not dst.is_cuda else 3
+    dev = dst.device if dst.is_cuda else src.device
+    nbytes = ctypes.c_int64(0)
+    _lib.check(lib.sigattn_copy_valid_rows(src.data_ptr(), dst.data_ptr(), B, H, N,
+                                           src.shape[-1] * src.element_size(), lens_h.data_ptr(),
+                                           1 if layout == "bshd" else 0, kind, _stream_handle(dev),
+                                           ctypes.byref(nbytes)))
+    return int(nbytes.value)
+
+
 def sigattn_permute_rows(x: torch.Tensor, index: torch.Tensor, scatter: bool) -> torch.Tensor:
     """[B, H, N, d] row gather (out[:, :, r] = x[:, :, index[r]]) or scatter (out[:, :, index[r]] = x[:, :, r])."""
     lib = _lib.load()

@@ -693,6 +693,34 @@ sigattn_status sigattn_permute_rows(const void* src, void* dst, const int32_t* i
   return SIGATTN_OK;
 }
 
+sigattn_status sigattn_copy_valid_rows(const void* src, void* dst, int B, int H, int N, int row_bytes,
+                                       const int32_t* host_lens, int layout_bshd, int kind, void* stream,
+                                       int64_t* bytes_out) {
+  if (!src || !dst || !host_lens || B <= 0 || H <= 0 || N <= 0 || row_bytes <= 0 || row_bytes % 16 != 0 ||
+      kind < 1 || kind > 3)
+    return fail(SIGATTN_EINVAL, "bad copy_valid_rows arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const cudaMemcpyKind k = static_cast<cudaMemcpyKind>(kind);
+  const size_t rb = (size_t)row_bytes, slab = (size_t)N * rb;
+  int64_t bytes = 0;
+  for (int b = 0; b < B; ++b) {
+    const int n = std::min(std::max(host_lens[b], 0), N);
+    if (n == 0) continue;
+    if (layout_bshd) {   // sequence b: rows [0, n) of all heads are one block of n * H rows
+      const size_t off = (size_t)b * N * H * rb, len = (size_t)n * H * rb;
+      CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, static_cast<const uint8_t*>(src) + off, len, k, s));
+      bytes += (int64_t)len;
+    } else {             // H slabs of N rows: n rows each, pitch N rows
+      const size_t off = (size_t)b * H * slab;
+      CUDA_TRY(cudaMemcpy2DAsync(static_cast<uint8_t*>(dst) + off, slab, static_cast<const uint8_t*>(src) + off, slab,
+                                 (size_t)n * rb, (size_t)H, k, s));
+      bytes += (int64_t)n * H * (int64_t)rb;
+    }
+  }
+  if (bytes_out) *bytes_out = bytes;
+  return SIGATTN_OK;
+}
+
 sigattn_status sigattn_mask_to_seqlens(const uint8_t* key_padding_mask, int B, int N, int32_t* seqlens,
                                        int32_t* nonprefix_flag, void* stream) {
   if (!key_padding_mask || !seqlens || !nonprefix_flag || B <= 0 || N <= 0)

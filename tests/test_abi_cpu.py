@@ -172,3 +172,24 @@ def test_c_program_links_against_header(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "abi_test: OK" in r.stdout
+
+
+def test_copy_valid_rows_rejects_bad_arguments():
+    """sigattn_copy_valid_rows validates its arguments before enqueueing any copy (no GPU needed)."""
+    lib = _lib.load()
+    lens = (ctypes.c_int32 * 2)(3, 1)
+    buf = ctypes.create_string_buffer(4096)
+    p = ctypes.cast(buf, ctypes.c_void_p).value
+    n = ctypes.c_int64(-1)
+    cases = [
+        dict(src=None), dict(dst=None), dict(lens=None), dict(B=0), dict(H=-1), dict(N=0),
+        dict(rb=24),   # row bytes not a multiple of 16
+        dict(kind=0), dict(kind=4),
+    ]
+    for c in cases:
+        a = dict(src=p, dst=p + 2048, B=2, H=1, N=4, rb=128, lens=ctypes.cast(lens, ctypes.c_void_p).value, kind=1)
+        a.update(c)
+        st = lib.sigattn_copy_valid_rows(a["src"], a["dst"], a["B"], a["H"], a["N"], a["rb"], a["lens"], 0,
+                                         a["kind"], None, ctypes.byref(n))
+        assert st == 1, c   # SIGATTN_EINVAL
+    assert n.value == -1, "no bytes reported on a rejected call"

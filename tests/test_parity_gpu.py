@@ -766,3 +766,48 @@ def test_pad_fill_many_slabs(d, layout):
         assert e <= BF16_TOL, f"{name} rel err {e}"
         for bb, n in enumerate(lens):
             assert (g[bb, :, n:] == 0).all(), f"{name}: padded rows of sequence {bb} not exactly 0"
+
+
+@pytest.mark.parametrize("layout", ["bhsd", "bshd"])
+def test_copy_valid_rows_roundtrip(layout):
+    """Padding-aware transfers (sigattn_copy_valid_rows): host -> device -> device -> host moves exactly
+    the valid rows (byte count = sum of n_b * H rows) and leaves every padded row of the destination
+    untouched; an attention step fed through them matches the padded-copy step bitwise."""
+    sa = _sa()
+    B, H, N, d = 5, 3, 300, 64
+    lens = [300, 0, 1, 129, 256]
+    shape = (B, N, H, d) if layout == "bshd" else (B, H, N, d)
+    g = torch.Generator().manual_seed(5)
+    src = torch.randn(shape, generator=g).to(torch.bfloat16).pin_memory()
+    dev = torch.full(shape, 7.0, dtype=torch.bfloat16, device="cuda")
+    nb = sa.copy_valid_rows(src, dev, lens, layout=layout)
+    assert nb == sum(lens) * H * d * 2
+    dev2 = torch.full_like(dev, 9.0)
+    sa.copy_valid_rows(dev, dev2, lens, layout=layout)
+    back = torch.full(shape, 5.0, dtype=torch.bfloat16).pin_memory()
+    sa.copy_valid_rows(dev2, back, lens, layout=layout)
+    torch.cuda.synchronize()
+    for b, n in enumerate(lens):
+        if layout == "bshd":
+            v_ref, v_dev, v_back = src[b, :n], dev[b, :n].cpu(), back[b, :n]
+            p_dev, p_back = dev[b, n:].cpu(), back[b, n:]
+        else:
+            v_ref, v_dev, v_back = src[b, :, :n], dev[b, :, :n].cpu(), back[b, :, :n]
+            p_dev, p_back = dev[b, :, n:].cpu(), back[b, :, n:]
+        assert torch.equal(v_dev, v_ref) and torch.equal(v_back, v_ref)
+        assert torch.all(p_dev == 7.0) and torch.all(p_back == 5.0), "padded rows must not be touched"
+    # an attention step through the valid-row path equals the padded-copy path
+    cfg = I.Config("e2e", B=4, H=2, N=320, d=64, lengths=[320, 129, 7, 0], seed=80)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    alpha, bias = 1 / 8, -math.log(320)
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    dq_, dk_, dv_ = (torch.zeros_like(t) for t in (q, k, v))
+    for h_, d_ in ((hq, dq_), (hk, dk_), (hv, dv_)):
+        sa.copy_valid_rows(h_, d_, cfg.nq)
+    o_valid = sa.sigattn_fwd(dq_, dk_, dv_, nq, nk, alpha, bias)
+    o_full = sa.sigattn_fwd(q, k, v, nq, nk, alpha, bias)
+    ho = torch.zeros(o_full.shape, dtype=o_full.dtype).pin_memory()
+    sa.copy_valid_rows(o_valid, ho, cfg.nq)
+    torch.cuda.synchronize()
+    assert torch.equal(o_valid, o_full), "outputs must not depend on padded input rows (R3)"
+    assert torch.equal(ho, o_full.cpu())
