@@ -42,7 +42,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -433,6 +433,8 @@ def main_ours(args):
     # (sa.copy_valid_rows, sigattn_copy_valid_rows): only the valid rows of each (b, h) slab cross
     # PCIe; the persistent device buffers' padded rows stay zero (zeroed once), and the host output
     # buffers' padded rows are zeroed once -- the padded output rows are exact zeros by contract.
+    # Three streams pipeline consecutive steps (upload of step i+1 and download of step i-1 run on
+    # the two copy engines while step i computes), double-buffered device inputs and outputs.
     e2e = None
     if not args.no_e2e:
         alpha, bias = wl.alpha, wl.bias
@@ -440,32 +442,55 @@ def main_ours(args):
         hnq, hnk = wl.nq.cpu().pin_memory(), wl.nk.cpu().pin_memory()
         lq, lk = hnq.tolist(), hnk.tolist()
         ho, hdq, hdk, hdv = (torch.zeros(t_.shape, dtype=t_.dtype).pin_memory() for t_ in (wl.q, wl.q, wl.k, wl.v))
-        dq_, dk_, dv_, ddo = (torch.zeros_like(t_) for t_ in (wl.q, wl.k, wl.v, wl.do))
-        oo, g1, g2, g3 = (torch.empty_like(t_) for t_ in (wl.q, wl.q, wl.k, wl.v))
-        snq, snk = torch.empty_like(wl.nq), torch.empty_like(wl.nk)
+        ins = [tuple(torch.zeros_like(t_) for t_ in (wl.q, wl.k, wl.v, wl.do)) for _ in range(2)]
+        outs = [tuple(torch.empty_like(t_) for t_ in (wl.q, wl.q, wl.k, wl.v)) for _ in range(2)]
+        lens_d = [(torch.empty_like(wl.nq), torch.empty_like(wl.nk)) for _ in range(2)]
+        s_in, s_c, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        done_in, done_c, done_out = {}, {}, {}
         moved = [0, 0]
 
-        def e2e_step():
-            h2d = sum(sa.copy_valid_rows(h_, d_, lens) for h_, d_, lens in
-                      ((hq, dq_, lq), (hk, dk_, lk), (hv, dv_, lk), (hdo, ddo, lq)))
-            snq.copy_(hnq, non_blocking=True)
-            snk.copy_(hnk, non_blocking=True)
-            sa.sigattn_fwd(dq_, dk_, dv_, snq, snk, alpha, bias, out=oo, workspace=wl.fws)
-            sa.sigattn_bwd(dq_, dk_, dv_, ddo, snq, snk, alpha, bias, dq=g1, dk=g2, dv=g3, workspace=wl.ws)
-            d2h = sum(sa.copy_valid_rows(d_, h_, lens) for d_, h_, lens in
-                      ((oo, ho, lq), (g1, hdq, lq), (g2, hdk, lk), (g3, hdv, lk)))
+        def e2e_step(i):
+            j = i % 2
+            (dq_, dk_, dv_, ddo), (oo, g1, g2, g3), (snq, snk) = ins[j], outs[j], lens_d[j]
+            with torch.cuda.stream(s_in):   # upload: set j is free once step i-2 computed
+                if i - 2 in done_c:
+                    s_in.wait_event(done_c[i - 2])
+                h2d = sum(sa.copy_valid_rows(h_, d_, lens) for h_, d_, lens in
+                          ((hq, dq_, lq), (hk, dk_, lk), (hv, dv_, lk), (hdo, ddo, lq)))
+                snq.copy_(hnq, non_blocking=True)
+                snk.copy_(hnk, non_blocking=True)
+                done_in[i] = ev()
+                done_in[i].record(s_in)
+            with torch.cuda.stream(s_c):    # compute: inputs landed, output set j downloaded (step i-2)
+                s_c.wait_event(done_in[i])
+                if i - 2 in done_out:
+                    s_c.wait_event(done_out[i - 2])
+                sa.sigattn_fwd(dq_, dk_, dv_, snq, snk, alpha, bias, out=oo, workspace=wl.fws)
+                sa.sigattn_bwd(dq_, dk_, dv_, ddo, snq, snk, alpha, bias, dq=g1, dk=g2, dv=g3, workspace=wl.ws)
+                done_c[i] = ev()
+                done_c[i].record(s_c)
+            with torch.cuda.stream(s_out):  # download
+                s_out.wait_event(done_c[i])
+                d2h = sum(sa.copy_valid_rows(d_, h_, lens) for d_, h_, lens in
+                          ((oo, ho, lq), (g1, hdq, lq), (g2, hdk, lk), (g3, hdv, lk)))
+                done_out[i] = ev()
+                done_out[i].record(s_out)
             moved[0] = h2d + hnq.numel() * hnq.element_size() + hnk.numel() * hnk.element_size()
             moved[1] = d2h
 
-        e2e_step()
+        for i in range(2):
+            e2e_step(i)
         torch.cuda.synchronize()
+        done_in.clear(), done_c.clear(), done_out.clear()
         if world > 1:
             dist.barrier()
         s2, t2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s2.record()
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        t2.record()
+        s2.record(s_in)
+        for i in range(args.e2e_steps):
+            e2e_step(i)
+        s_in.wait_stream(s_out)
+        t2.record(s_in)
         torch.cuda.synchronize()
         e_ms = torch.tensor([s2.elapsed_time(t2) / args.e2e_steps], dtype=torch.float64, device=dev)
         if world > 1:
@@ -474,7 +499,8 @@ def main_ours(args):
                "h2d_bytes_per_step": int(moved[0]), "d2h_bytes_per_step": int(moved[1]),
                "ms_per_step": float(e_ms.item()), "steps": args.e2e_steps,
                "path": "pinned host -> copy_valid_rows (valid rows of Q, K, V, dO) -> sigattn_fwd/sigattn_bwd "
-                       "(public API) -> copy_valid_rows -> pinned host (O, dQ, dK, dV); padded rows never cross PCIe"}
+                       "(public API) -> copy_valid_rows -> pinned host (O, dQ, dK, dV); padded rows never cross "
+                       "PCIe; upload / compute / download of consecutive steps pipelined on three streams"}
 
     peak, peak_sus, peak_src = load_peaks()
     bwd_tflops = wl.rank_bwd_flops / (bwd_ms * 1e-3) / 1e12
