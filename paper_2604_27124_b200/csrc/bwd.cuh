@@ -576,7 +576,9 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             const uint32_t dsr = ds_row + (t & 1) * C::kDSBytes + qh * (kTile * 128);
             sm100::st_shared_v4(dsr + (((2 * w4) ^ (row & 7)) * 16), dd[0], dd[1], dd[2], dd[3]);
             sm100::st_shared_v4(dsr + (((2 * w4 + 1) ^ (row & 7)) * 16), dd[4], dd[5], dd[6], dd[7]);
-            sm100::fence_proxy_async_smem();
+            // the dQ MMA reading both halves is issued after p_full[1]: one proxy fence there orders
+            // this thread's stores of both halves
+            if (qh == 1) sm100::fence_proxy_async_smem();
           }
           sm100::tmem_wait_st();
           sm100::tc_fence_before();
