@@ -30,12 +30,15 @@
 #ifndef SIGATTN_DBG_MMAONLY
 #define SIGATTN_DBG_MMAONLY 0       // backward: MMA + TMA pipeline alone (no compute / epilogue waits)
 #endif
+#ifndef SIGATTN_DBG_EPI_NOSTORE
+#define SIGATTN_DBG_EPI_NOSTORE 0   // two-tile forward: the O epilogue skips its global stores
+#endif
 #ifndef SIGATTN_DBG_NOFILL
 #define SIGATTN_DBG_NOFILL 0        // fwd / bwd: skip the padded-row zero fills (outputs incomplete)
 #endif
 
 #if !defined(SIGATTN_DEBUG_BUILD) &&                                                                     \
     (SIGATTN_DBG_FWD_NOSIGMA || SIGATTN_DBG_FWD_NOTMA_KV || SIGATTN_DBG_NOCOMPUTE || SIGATTN_DBG_EPI_NOLD || \
-     SIGATTN_DBG_NORED || SIGATTN_DBG_NOSTAGE || SIGATTN_DBG_NOTMA_QDO || SIGATTN_DBG_MMAONLY || SIGATTN_DBG_NOFILL)
+     SIGATTN_DBG_NORED || SIGATTN_DBG_NOSTAGE || SIGATTN_DBG_NOTMA_QDO || SIGATTN_DBG_MMAONLY || SIGATTN_DBG_NOFILL || SIGATTN_DBG_EPI_NOSTORE)
 #error "SIGATTN_DBG_* switches make the kernels compute wrong results: timing builds only (-DSIGATTN_DEBUG_BUILD)"
 #endif

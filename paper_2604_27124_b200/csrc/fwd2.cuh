@@ -36,7 +36,11 @@ struct Fwd2Cfg {
   // d = 64: P gets its own TMEM columns so a pair releases S_x(j) once it has READ it (mid-sigma)
   // and S_x(j+1) is computed while the pair still works on sigma(j); d = 128 has no room (P aliased).
   static constexpr bool kSepP = (D == 64);
-  static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 1024;
+  // d = 128: per sigma warp a 2 KB staging tile (32 rows x 32 columns of 16-bit O) through which
+  // the epilogue turns row-per-lane stores into 64-byte row segments (8 rows per store instruction)
+  static constexpr int kStgOff = (kBarOff + kNumBars * 8 + 16 + 127) / 128 * 128;
+  static constexpr int kStgBytes = (D == 128) ? 16 * 2048 : 0;
+  static constexpr int kSmemBytes = kStgOff + kStgBytes + 1024;
   static constexpr int kWarpTMA = 16, kWarpMMA = 17, kWarpAlloc = 18, kWarpFill = 19;
   static constexpr int kThreads = 32 * 20;
   static constexpr uint32_t kTmemCols = 512;
@@ -366,7 +370,33 @@ sigattn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             dst[e >> 2] = valid ? make_float4(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1]),
                                               __uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3]))
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        } else if (qrow < args.Nq) {
+        } else if (C::kStgBytes > 0 && !kOutF32) {
+          // stage the warp's 32 rows x 32 columns (64 bytes per row; 16-byte chunk c of row r at slot
+          // c ^ ((r >> 1) & 3): conflict-free both ways), then store 8 rows x 64 bytes per instruction
+          const uint32_t stg = sm100::smem_u32(smem + C::kStgOff + warp * 2048);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int e = 8 * c;
+            sm100::st_shared_v4(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) * 16),
+                                sm100::pack2<kBf16>(__uint_as_float(ov[e + 0]), __uint_as_float(ov[e + 1])),
+                                sm100::pack2<kBf16>(__uint_as_float(ov[e + 2]), __uint_as_float(ov[e + 3])),
+                                sm100::pack2<kBf16>(__uint_as_float(ov[e + 4]), __uint_as_float(ov[e + 5])),
+                                sm100::pack2<kBf16>(__uint_as_float(ov[e + 6]), __uint_as_float(ov[e + 7])));
+          }
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int rr = 8 * k + (int)(lane >> 2), cc = (int)(lane & 3);
+            const uint4 w = sm100::ld_shared_v4(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
+            const int grow = qt * kTile + (int)quarter * 32 + rr;
+            if (grow < args.Nq && !SIGATTN_DBG_EPI_NOSTORE) {
+              const uint4 z = grow < nq ? w : make_uint4(0u, 0u, 0u, 0u);
+              *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) +
+                                        row_off(args.bshd, args.H, args.Nq, D, b, h, grow) + c0 + cc * 8) = z;
+            }
+          }
+          __syncwarp();   // the next piece overwrites the staging tile
+        } else if (qrow < args.Nq && !SIGATTN_DBG_EPI_NOSTORE) {
           if constexpr (kOutF32) {
             float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + rowoff + c0);
 #pragma unroll
