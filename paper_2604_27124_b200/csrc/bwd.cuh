@@ -556,11 +556,13 @@ sigattn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
           const int nv = full ? 16 : (key_valid ? ncol : 0);
           if (full) bwd_sigma16<false, false>(s, a2, b2, true, 16, tmem + lane_addr + s_col, spec);
           else bwd_sigma16<true, false>(s, a2, b2, key_valid, nv, tmem + lane_addr + s_col, spec);
+          if (qh == 0) BWD_TR(6);
           // dP^T(t, q) lands after S^T(t, q): sigma above overlaps the dP^T MMAs
           SIGATTN_COMPUTE_WAIT(&dp_full[qh], t & 1);
           sm100::tc_fence_after();
           sm100::tmem_ld16(tmem + lane_addr + dp_col, dp);
           sm100::tmem_wait_ld_dep16(dp);
+          if (qh == 0) BWD_TR(7);
           uint32_t pp[8], dd[8];
           if (full) bwd_ds16<false, kBf16, kDB>(s, dp, pp, dd, 16, &db_acc);
           else bwd_ds16<true, kBf16, kDB>(s, dp, pp, dd, nv, &db_acc);

@@ -82,7 +82,8 @@ for cta in range(148):
         put("MMA j dQ(t) issued", r[1536 + t])
         put("MMA k next p_full0", r[t + 1])
         ev = r[2048:3072].reshape(16, 8, 8)[:, t - 40, :]
-        for e, nm in enumerate(["S h0 seen", "h0 done", "h0 arrived", "S h1 seen", "h1 done", "h1 arrived"]):
+        for e, nm in enumerate(["S h0 seen", "h0 done", "h0 arrived", "S h1 seen", "h1 done", "h1 arrived",
+                                "h0 sigma done", "h0 dP loaded"]):
             vals = ev[:, e]
             if (vals > 0).all():
                 put("cmp first " + nm, vals.min())
