@@ -811,3 +811,28 @@ def test_copy_valid_rows_roundtrip(layout):
     torch.cuda.synchronize()
     assert torch.equal(o_valid, o_full), "outputs must not depend on padded input rows (R3)"
     assert torch.equal(ho, o_full.cpu())
+
+
+def test_pad_fill_many_slabs_no_zero_pad_out():
+    """SIGATTN_F_NO_ZERO_PAD_OUT through the rewritten fill (pad_rows = 0: only the valid rows of
+    sequences with an empty key set are written, as exact zeros) at 144 slabs: padded rows keep the
+    caller's NaN, every valid row matches the oracle."""
+    sa = _sa()
+    lq = [0, 1, 127, 128, 129, 255, 384, 300] * 3
+    lk = [384, 0, 0, 128, 200, 0, 384, 1] * 3
+    cfg = I.Config("fill_nz", B=24, H=6, N=384, d=64, lengths=lq, Nk=384, lengths_k=lk, seed=77)
+    q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
+    alpha, b = 1.0 / 8, -math.log(384)
+    o = sa.sigattn_fwd(q, k, v, nq, nk, alpha, b, out=torch.full_like(q, float("nan")), zero_pad_out=False)
+    torch.cuda.synchronize()
+    ro = oracle.fwd(f64(q), f64(k), f64(v), cfg.nq, cfg.nk, alpha, np.full(cfg.B, b))
+    g = f64(o)
+    for bb, (n, m) in enumerate(zip(lq, lk)):
+        valid = g[bb, :, :n]
+        assert np.isfinite(valid).all(), f"valid rows of sequence {bb} not written"
+        assert np.abs(valid - ro[bb, :, :n]).max(initial=0) <= BF16_TOL * np.abs(ro).max()
+        if m == 0:
+            assert (valid == 0).all(), "n_k = 0: valid O rows are exact zeros"
+        # rows past the last valid 128-row tile are never written with the flag
+        r1 = min((n + 127) // 128 * 128, 384) if n > 0 and m > 0 else n
+        assert np.isnan(g[bb, :, r1:]).all(), f"padded rows of sequence {bb} must be left untouched"
