@@ -231,12 +231,15 @@ def test_c3_full_size_sampled():
 
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("bias,scale", [(0.0, None), (3.0, None), (-1.0, 0.5), (-30.0, None), (-3.2, 0.02),
-                                        (-4.6, 0.01), (-5.5, None)])
+                                        (-4.6, 0.01), (-5.5, None), (-8.5, 0.5), (-12.0, 1.0)])
 def test_sigmoid_slow_and_saturated_paths(bias, scale, d):
     """Logits above -2 (bias 0 / +3 / large scale) exercise the exact-range sigma path; logits in
     (-4, -2] the quadratic tier (bias -3.2, scale 0.02); <= -4 the linear tier (bias -4.6); bias -5.5
     with unit-variance logits fails the tier-4 vote in some chunks only (speculation on/off per warp);
-    bias -30 saturates to P ~ 0.  Both kernels, d = 64 and 128, must stay within the bf16 bound."""
+    bias -30 saturates to P ~ 0.  Biases <= -8.3 make the forward and the d = 128 backward speculate
+    the <= -4 tier (kSpec4MaxBias); with large scales (-8.5 / 0.5, -12 / 1.0) that speculation fails
+    in many chunks (reload from TMEM, exact tiers).  Both kernels, d = 64 and 128, must stay within the
+    bf16 bound."""
     sa = _sa()
     cfg = I.Config("slowpath", B=2, H=2, N=256, d=d, lengths=[256, 150], seed=21)
     q, k, v, do, nq, nk = I.make_inputs(cfg, "cuda")
