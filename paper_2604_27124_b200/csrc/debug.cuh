@@ -21,9 +21,6 @@
 #ifndef SIGATTN_DBG_NORED
 #define SIGATTN_DBG_NORED 0         // backward: no dQ reduce-add into global memory
 #endif
-#ifndef SIGATTN_DBG_NOSTAGE
-#define SIGATTN_DBG_NOSTAGE 0       // backward: epilogue skips the dS shared-memory staging
-#endif
 #ifndef SIGATTN_DBG_NOTMA_QDO
 #define SIGATTN_DBG_NOTMA_QDO 0     // backward: Q/dO tiles loaded once, then reused (stale)
 #endif
@@ -39,6 +36,6 @@
 
 #if !defined(SIGATTN_DEBUG_BUILD) &&                                                                     \
     (SIGATTN_DBG_FWD_NOSIGMA || SIGATTN_DBG_FWD_NOTMA_KV || SIGATTN_DBG_NOCOMPUTE || SIGATTN_DBG_EPI_NOLD || \
-     SIGATTN_DBG_NORED || SIGATTN_DBG_NOSTAGE || SIGATTN_DBG_NOTMA_QDO || SIGATTN_DBG_MMAONLY || SIGATTN_DBG_NOFILL || SIGATTN_DBG_EPI_NOSTORE)
+     SIGATTN_DBG_NORED || SIGATTN_DBG_NOTMA_QDO || SIGATTN_DBG_MMAONLY || SIGATTN_DBG_NOFILL || SIGATTN_DBG_EPI_NOSTORE)
 #error "SIGATTN_DBG_* switches make the kernels compute wrong results: timing builds only (-DSIGATTN_DEBUG_BUILD)"
 #endif
