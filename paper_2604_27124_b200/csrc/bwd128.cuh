@@ -156,22 +156,30 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     const uint32_t q_base = sm100::smem_u32(smem + C::kQOff);
     const uint32_t do_base = sm100::smem_u32(smem + C::kDOOff);
     const uint32_t ds_base = sm100::smem_u32(smem + C::kDSOff);
-    auto mma_s = [&](uint32_t st) {
-      const uint32_t qa = q_base + st * C::kQBytes, da = do_base + st * C::kQBytes;
+    // S^T then dP^T, each on its own barrier: the compute warps start sigma while dP^T is computed
+    auto mma_s_only = [&](uint32_t st) {
+      const uint32_t qa = q_base + st * C::kQBytes;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const uint32_t ko = (kk >> 2) * (kTile * 128) + (kk & 3) * 32, qo = (kk >> 2) * (C::kQT * 128) + (kk & 3) * 32;
         sm100::mma_ss(tmem + C::kColS, sm100::sdesc_add(sm100::make_sdesc_sw128(k_base, 16, 1024), ko),
                       sm100::sdesc_add(sm100::make_sdesc_sw128(qa, 16, 1024), qo), idesc_s, kk > 0);
       }
+      sm100::mma_commit(s_full);
+    };
+    auto mma_dp_only = [&](uint32_t st) {
+      const uint32_t da = do_base + st * C::kQBytes;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
-        if (kk == 0) sm100::mma_commit(s_full);   // the compute warps start sigma while dP^T is computed
         const uint32_t ko = (kk >> 2) * (kTile * 128) + (kk & 3) * 32, qo = (kk >> 2) * (C::kQT * 128) + (kk & 3) * 32;
         sm100::mma_ss(tmem + C::kColDP, sm100::sdesc_add(sm100::make_sdesc_sw128(v_base, 16, 1024), ko),
                       sm100::sdesc_add(sm100::make_sdesc_sw128(da, 16, 1024), qo), idesc_s, kk > 0);
       }
       sm100::mma_commit(dp_full);
+    };
+    auto mma_s = [&](uint32_t st) {
+      mma_s_only(st);
+      mma_dp_only(st);
     };
     auto mma_dq = [&](uint32_t buf) {
       const uint32_t dsa = ds_base + buf * C::kDSBytes;
@@ -200,13 +208,28 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sm100::mbar_wait_backoff(p_full, t & 1);
         if (i == 0) sm100::mbar_wait(acc_empty, (item_c & 1) ^ 1);
         sm100::tc_fence_after();
+        // dV(i) | S(i+1) | dK(i) | dP(i+1) | dQ(i): S(i+1) overwrites the S^T columns right after dV(i)
+        // has read P^T(i) from them, dP(i+1) the dP^T columns after dK(i) has read dS^T(i) (in-order
+        // tcgen05 execution), so the compute warps get the next scores four MMAs earlier
+        const bool has_next_here = i + 1 < nqt;
+        const uint32_t st1 = (t + 1) % C::kQStages;
         if (sm100::elect_one()) {
-          const uint32_t qa = q_base + st * C::kQBytes, da = do_base + st * C::kQBytes;
+          const uint32_t da = do_base + st * C::kQBytes;
 #pragma unroll
           for (int kk = 0; kk < C::kQT / 16; ++kk)   // dV += P^T dO  (queries 16kk: warpgroup kk's columns)
             sm100::mma_ts(tmem + C::kColDV, tmem + C::kColS + kk * 16,
                           sm100::sdesc_add(sm100::make_sdesc_sw128(da, C::kQT * 128, 1024), kk * 2048), idesc_acc,
                           (i == 0 && kk == 0) ? 0u : 1u);
+        }
+        __syncwarp();
+        if (has_next_here) {
+          sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
+          sm100::tc_fence_after();
+          if (sm100::elect_one()) mma_s_only(st1);
+          __syncwarp();
+        }
+        if (sm100::elect_one()) {
+          const uint32_t qa = q_base + st * C::kQBytes;
 #pragma unroll
           for (int kk = 0; kk < C::kQT / 16; ++kk)   // dK += dS^T Q
             sm100::mma_ts(tmem + C::kColDK, tmem + C::kColDP + kk * 16,
@@ -215,16 +238,9 @@ sigattn_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
           sm100::mma_commit(&qdo_empty[st]);
           if (i == nqt - 1) sm100::mma_commit(acc_full);
           if (i == 0 && args.counters) atomicAdd(args.counters + 1, (unsigned long long)nqt);
+          if (has_next_here) mma_dp_only(st1);
         }
         __syncwarp();
-        const bool has_next_here = i + 1 < nqt;
-        if (has_next_here) {     // next tile's scores before dQ(i)
-          const uint32_t st1 = (t + 1) % C::kQStages;
-          sm100::mbar_wait(&qdo_full[st1], ((t + 1) / C::kQStages) & 1);
-          sm100::tc_fence_after();
-          if (sm100::elect_one()) mma_s(st1);
-          __syncwarp();
-        }
         if constexpr (kDQ) {
           sm100::mbar_wait(dq_empty, (t & 1) ^ 1);
           sm100::tc_fence_after();
